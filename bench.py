@@ -1,0 +1,333 @@
+"""bench.py -- seconds per outer iteration of CCD++ (and ALS) at synthetic Netflix shape, k=40.
+
+BASELINE.json metric: "sec/outer-iter (CCD++, ALS) at Netflix shape k=40, %HBM peak; RMSE vs CPU ref".
+A "step" is one outer iteration (ccd.hpp:370-398): for t in 0..k-1 the rank-one step (fused
+promote, 15 x (u-sweep, v-sweep), deferred writeback).  Workload = BASELINE configs[2] (CCD++ k=40
+on the 480,189 x 17,770 synthetic Netflix shape, 99,072,112 training ratings + 1,408,395 probe);
+the ALS configs[3] number on the same data is reported under "als".
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config NAME]
+
+Multi-GPU: launched by torch.distributed.run, one process per GPU; each rank owns a CSR row block and
+a CSC column block (strong scaling of the fixed Netflix problem); u/v are all-gathered over NCCL.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # name: (m, n, n_train, n_probe, k, lambda, inner, solver)
+    "netflix-ccdpp": (480189, 17770, 99072112, 1408395, 40, 0.05, 15, "ccdpp"),
+    "netflix-als": (480189, 17770, 99072112, 1408395, 40, 0.05, 1, "als"),
+    "yahoo-ccdpp": (1000990, 624961, 252800275, 4003960, 100, 0.05, 15, "ccdpp"),
+    "ml10m-als": (69878, 10677, 9900000, 100000, 10, 0.05, 1, "als"),
+    "ml100k-ccdpp": (943, 1682, 90000, 10000, 10, 0.05, 15, "ccdpp"),
+}
+GEN_SEED, MODEL_SEED = 777, 1
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.proc, self.lines = device, None, []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = max(mx, float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def make_data(cfg_name):
+    import paper_1511_02433_b200 as P
+    m, n, ntr, npr, *_ = CONFIGS[cfg_name]
+    t0 = time.perf_counter()
+    train, probe = P.synth_ratings(m, n, 3, ntr, npr, GEN_SEED)
+    A = P.RatingsMatrix.from_triplets(train, m, n)
+    log(f"[bench] data {cfg_name}: {m}x{n} nnz={A.nnz()} probe={len(probe)} in {time.perf_counter() - t0:.1f}s")
+    return train, probe, A
+
+
+def ccd_bytes(N, m, n, k, T):
+    """SURVEY.md 8(d) algorithmic bytes (FP32 values, int32 indices, int64 offsets)."""
+    u = 8 * N + 12 * m + 4 * n
+    v = 8 * N + 12 * n + 4 * m
+    per_iter = k * (T * (16 * N + 16 * (m + n)) + 8 * N)
+    return u, v, per_iter
+
+
+def cpu_reference_ccdpp(train, m, n, k, lam, inner, steps, workers):
+    """The reference CPU path (oracle/_ref = parmf headers compiled here), timed on a bounded sample:
+    `steps` rank-one steps of a steady-state (W != 0) outer iteration on the full matrix."""
+    from oracle.pyoracle import Reference
+    R = Reference()
+    t0 = time.perf_counter()
+    M = R.matrix(train, m, n, "_f32")
+    log(f"[bench] reference RatingsMatrix::from_triplets {time.perf_counter() - t0:.1f}s")
+    per_step = M.ccdpp_sample(k, lam, inner, workers, steps, MODEL_SEED)
+    return M, per_step
+
+
+def run_ours(args, rank, world, dist):
+    import paper_1511_02433_b200 as P
+    cfg_name = args.config
+    m, n, ntr, npr, k, lam, inner, solver = CONFIGS[cfg_name]
+    device = int(os.environ.get("LOCAL_RANK", "0"))
+    train, probe, A = make_data(cfg_name)
+    N = A.nnz()
+    nccl_id = None
+    if world > 1:
+        import torch.distributed as td
+        obj = [P.nccl_unique_id() if rank == 0 else None]
+        td.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    t0 = time.perf_counter()
+    ctx = P.Context(A, device=device, rank=rank, world=world, nccl_id=nccl_id)
+    log(f"[bench] context (layouts + upload) {time.perf_counter() - t0:.1f}s")
+    ctx.set_probe(probe)
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    res = {}
+    if solver == "ccdpp":
+        cfg = P.CcdConfig(k=k, lam=lam, outer_iters=max(1, args.steps), inner_iters=inner, seed=MODEL_SEED)
+        ctx.ccdpp_begin(cfg)
+        iterate = ctx.ccdpp_iterate
+    else:
+        cfg = P.AlsConfig(k=k, lam=lam, outer_iters=max(1, args.steps), seed=MODEL_SEED)
+        ctx.als_begin(cfg)
+        iterate = ctx.als_iterate
+    iterate(args.warmup)
+    barrier(dist)
+    with ClockSampler(device) as clk:
+        secs = iterate(args.steps)
+    times = [max_over_ranks(dist, s) for s in secs]
+    launches = ctx.launch_count()
+    obj, rmse, trmse = ctx.metrics()
+    value = float(np.mean(times))
+    res.update(value=value, times=times, launches=launches, objective=obj, rmse=rmse, train_rmse=trmse,
+               clocks=clk.summary())
+    roof = None
+    if solver == "ccdpp":
+        ub, vb, per_iter = ccd_bytes(N, m, n, k, inner)
+        ctx.set_profiling(True)
+        iterate(1)
+        st = ctx.kernel_stats()
+        ctx.set_profiling(False)
+        # per launch: the 15 sweeps of a step, the first one with the promote RMW (+4N)
+        u_bytes = st["usweep_launches"] * ub + k * 4 * N
+        v_bytes = st["vsweep_launches"] * vb + k * 4 * N
+        u_ach = u_bytes / (st["usweep_ms"] * 1e-3) / 1e9
+        v_ach = v_bytes / (st["vsweep_ms"] * 1e-3) / 1e9
+        dom = "v-sweep" if st["vsweep_ms"] >= st["usweep_ms"] else "u-sweep"
+        ach = v_ach if dom == "v-sweep" else u_ach
+        traffic = None
+        try:
+            tr = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            traffic = tr.get(cfg_name, {}).get(dom)
+        except Exception:
+            pass
+        roof = {"bound": "hbm", "kernel": dom, "achieved": round(ach, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(ach / hbm, 4), "traffic": traffic,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (of measured)",
+                "whole_iteration": {"achieved": round(per_iter / value / 1e9, 1),
+                                    "frac": round(per_iter / value / 1e9 / hbm, 4),
+                                    "algorithmic_bytes_per_iter": per_iter},
+                "usweep": {"ms": st["usweep_ms"], "launches": st["usweep_launches"], "gbs": round(u_ach, 1)},
+                "vsweep": {"ms": st["vsweep_ms"], "launches": st["vsweep_launches"], "gbs": round(v_ach, 1)}}
+    res["roofline"] = roof
+    res["ctx"] = ctx
+    res["A"], res["probe"], res["train"] = A, probe, train
+    return res
+
+
+def barrier(dist):
+    if dist:
+        import torch.distributed as td
+        td.barrier()
+
+
+def max_over_ranks(dist, x):
+    if not dist:
+        return float(x)
+    import torch
+    import torch.distributed as td
+    t = torch.tensor([float(x)], dtype=torch.float64)
+    td.all_reduce(t, op=td.ReduceOp.MAX)
+    return float(t.item())
+
+
+def e2e_ours(args, A, probe):
+    """The public API end to end: pmf_ccdpp_train / pmf_als_train on HOST buffers (upload, device layout
+    build, K outer iterations with per-iteration metrics, model download) timed on the host clock."""
+    import paper_1511_02433_b200 as P
+    m, n, ntr, npr, k, lam, inner, solver = CONFIGS[args.config]
+    K = max(1, args.steps)
+    t0 = time.perf_counter()
+    if solver == "ccdpp":
+        model, rep = P.ccdpp_train(P.CcdConfig(k=k, lam=lam, outer_iters=K, inner_iters=inner, seed=MODEL_SEED), A,
+                                   probe)
+    else:
+        model, rep = P.als_train(P.AlsConfig(k=k, lam=lam, outer_iters=K, seed=MODEL_SEED), A, probe)
+    wall = time.perf_counter() - t0
+    return {"value": wall / K, "unit": "s/outer-iter", "h2d_bytes_per_step": int(rep.h2d_bytes / K),
+            "d2h_bytes_per_step": int(rep.d2h_bytes / K), "setup_seconds": round(rep.setup_seconds, 3),
+            "final_rmse": rep.final_rmse}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="netflix-ccdpp", choices=sorted(CONFIGS))
+    ap.add_argument("--cpu-steps", type=int, default=2, help="rank-one steps in the CPU reference sample")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-als", action="store_true")
+    args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    dist = world > 1
+    if dist:
+        import torch.distributed as td
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        td.init_process_group("gloo")
+    m, n, ntr, npr, k, lam, inner, solver = CONFIGS[args.config]
+    cores = os.cpu_count() or 1
+    unit = "s/outer-iter"
+    workload = {"workload": f"{solver}-{args.config.split('-')[0]}-k{k}", "m": m, "n": n, "nnz_train": ntr,
+                "probe": npr, "k": k, "lambda": lam, "inner_iters": inner if solver == "ccdpp" else None,
+                "solver": solver, "data": f"synthetic synth_ratings recipe, seed {GEN_SEED}, model seed {MODEL_SEED}",
+                "l2": "inputs larger than L2 (CSR+CSC residual ~1.6 GB >> 126 MB L2), no flush needed",
+                "parallelism": f"row/col blocks x{args.gpus}"}
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        import paper_1511_02433_b200 as P
+        train, probe, A = make_data(args.config)
+        if solver == "ccdpp":
+            from oracle.pyoracle import Reference
+            M = Reference().matrix(train, m, n, "_f32")
+            M.ccdpp_sample(k, lam, inner, cores, max(1, args.warmup), MODEL_SEED)
+            vals = [k * M.ccdpp_sample(k, lam, inner, cores, args.cpu_steps, MODEL_SEED) for _ in range(args.steps)]
+            sample = (f"{args.cpu_steps} of {k} rank-one steps per outer iteration (build + {inner}x(u,v) + writeback), "
+                      f"full matrix, steady state W != 0, extrapolated x{k}")
+        else:
+            from oracle.pyoracle import Reference
+            M = Reference().matrix(train, m, n, "_f32")
+            vals = [M.als_sample(k, lam, cores, 1, MODEL_SEED) for _ in range(args.steps)]
+            sample = "one full ALS epoch (W then H phase) per step"
+        v = float(np.mean(vals))
+        line = {"impl": "reference", "metric": f"sec/outer-iter {solver} (lower is better)", "value": v, "unit": unit,
+                "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
+                "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+                "data": "synthetic", "config": workload,
+                "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "reference", "sample": sample},
+                "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    res = run_ours(args, rank, world, dist)
+    als = None
+    if solver == "ccdpp" and not args.no_als and args.config == "netflix-ccdpp":
+        ctx = res["ctx"]
+        ctx.als_begin(__import__("paper_1511_02433_b200").AlsConfig(k=k, lam=lam, outer_iters=1, seed=MODEL_SEED))
+        ctx.als_iterate(1)
+        barrier(dist)
+        ts = [max_over_ranks(dist, s) for s in ctx.als_iterate(max(1, args.steps))]
+        o, r, t = ctx.metrics()
+        als = {"metric": "sec/outer-iter ALS k=40 Netflix shape", "value": float(np.mean(ts)), "unit": unit,
+               "launches_per_iter": ctx.launch_count(), "objective": o, "rmse": r}
+    e2e = None
+    if not args.no_e2e and not dist:
+        res["ctx"].close()
+        e2e = e2e_ours(args, res["A"], res["probe"])
+    cpu = None
+    if rank == 0 and not dist and not args.no_cpu_baseline and solver == "ccdpp":
+        try:
+            M, per_step = cpu_reference_ccdpp(res["train"], m, n, k, lam, inner, args.cpu_steps, cores)
+            cpu = {"value": k * per_step, "unit": unit, "cores": cores, "kind": "reference",
+                   "sample": f"{args.cpu_steps} of {k} rank-one steps (build + {inner}x(u,v) + writeback) on the "
+                             f"full matrix from a steady-state model, parmf ccdpp stage API with {cores} workers, "
+                             f"extrapolated x{k}"}
+        except Exception as e:  # reference library missing on this box
+            cpu = {"value": None, "unit": unit, "cores": cores, "kind": "reference", "sample": f"unavailable: {e}"}
+    if rank != 0:
+        return
+    v = res["value"]
+    line = {"metric": f"sec/outer-iter {solver} (lower is better)", "value": v, "unit": unit, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3, "higher_is_better": False,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic", "config": workload,
+            "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": e2e,
+            "gpu_launches": int(res["launches"] * args.steps), "clocks": res["clocks"],
+            "quality": {"objective": res["objective"], "probe_rmse": res["rmse"], "train_rmse": res["train_rmse"]},
+            "per_step_s": res["times"], "als": als}
+    print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

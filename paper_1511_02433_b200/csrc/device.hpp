@@ -1,0 +1,101 @@
+// device.hpp -- device-side data structures and kernel launchers shared by the .cu files.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "layout.hpp"
+
+namespace pmfgpu {
+
+// Device copy of one sweep layout (layout.hpp SweepLayout).
+struct DevSweep {
+    int32_t n_out = 0, gat_extent = 0, panel_size = 0, n_panels = 0, sentinel = 0;
+    bool smem = true, idx16 = true;
+    int64_t n_entries = 0;
+    int32_t n_units = 0, n_mo = 0, ctas = 0, n_slots = 0;
+    void* idx = nullptr;          // uint16_t* or int32_t*
+    float* R = nullptr;           // residual values (padded layout)
+    Unit* units = nullptr;
+    int32_t* unit_panel = nullptr;
+    Piece* pieces = nullptr;
+    int32_t* piece_start = nullptr;
+    int32_t* panel_base = nullptr;
+    int32_t* mo_out = nullptr;
+    int32_t* mo_start = nullptr;
+    float2* partial = nullptr;
+};
+
+enum SweepMode { kPlain = 0, kPromote = 1, kDemote = 2 };
+
+// Operands of one sweep.  "g*" vectors are indexed by the gather index (padded space),
+// "o*" vectors by the output index (out_off + local output).
+struct SweepOperands {
+    const float* gn = nullptr;  // num/den vector (v on the CSR side, u on the CSC side)
+    const float* ga = nullptr;  // demote factor, gathered   (v' on CSR, u' on CSC)
+    const float* gb = nullptr;  // promote factor, gathered  (h  on CSR, w  on CSC)
+    const float* oa = nullptr;  // demote factor, per output (u' on CSR, v' on CSC)
+    const float* ob = nullptr;  // promote factor, per output(w  on CSR, h  on CSC)
+    float* out = nullptr;       // result vector (u or v), written at out_off + o
+    int32_t out_off = 0;
+    float lambda = 0.f;
+};
+
+// Launches one CCD++ sweep over a layout (ccd.hpp:153-197 with the promote of ccd.hpp:133-151
+// and the deferred writeback of ccd.hpp:199-218 fused in when mode == kPromote; kDemote only
+// applies R -= oa*ga).  csr_side selects which operand is "w" (the skip test of ccd.hpp:142).
+// Also launches the fixed-order finalize for outputs with several units.  Returns the number of
+// kernels launched.
+int launch_sweep(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOperands& op,
+                 cudaStream_t stream);
+size_t sweep_smem_bytes(const DevSweep& L, SweepMode mode, bool csr_side);
+void sweep_set_attributes(size_t max_smem);
+
+// ---- evaluation (model.hpp:103-167) -----------------------------------------------------------
+// Factor element (i, t) lives at F[i * si + t * st].
+struct FactorView {
+    const float* p;
+    int64_t si, st;
+};
+
+// Per-unit squared-error sums of the CSR layout `L` (values A) into unit_loss[n_units].
+void launch_unit_loss(const DevSweep& L, const float* A, int32_t row_off, FactorView W,
+                      FactorView H, int k, double* unit_loss, cudaStream_t stream);
+// sum of squares of x[0..n) (double) into *out via a fixed-shape reduction (scratch >= 1024).
+void launch_sumsq(const float* x, int64_t n, double* scratch, double* out, cudaStream_t stream);
+// deterministic sum of x[0..n) into *out.
+void launch_sum(const double* x, int64_t n, double* scratch, double* out, cudaStream_t stream);
+struct DevTriplet {
+    int32_t user, item;
+    float rating;
+};
+// sum over probe of (r - predict)^2, predict in FP32 sequential t (model.hpp:103-114).
+void launch_probe_sse(const DevTriplet* probe, int64_t n, FactorView W, FactorView H, int k,
+                      double* scratch, double* out, cudaStream_t stream);
+
+// ---- ALS (als.hpp:47-68, dense.hpp:35-124) ------------------------------------------------------
+struct DevAls {
+    int32_t n_out = 0, n_units = 0, n_mo = 0, n_slots = 0, n_empty = 0;
+    int64_t n_entries = 0;
+    int32_t* idx = nullptr;
+    float* val = nullptr;
+    Unit* units = nullptr;
+    int32_t* mo_out = nullptr;
+    int32_t* mo_start = nullptr;
+    int32_t* empty_out = nullptr;
+    float* partial = nullptr;   // n_slots * (k*k + k)
+};
+
+// Solves every output row of one side: out row (out_off + o) of the row-major factor `out`
+// (stride k) from the row-major opposing factor `opp`.  status: device int set to 4 on a
+// non-positive pivot.  Returns kernels launched.
+int launch_als_half(const DevAls& L, const float* opp, float* out, int32_t out_off, int k,
+                    float lambda, bool weighted, int* d_counter, int* d_status, int sm_count,
+                    cudaStream_t stream);
+void als_set_attributes();
+// Batched Cholesky factor + solve of `batch` k*k row-major systems in place.
+void launch_cholesky_batched(float* a, float* x, int batch, int k, int* d_status,
+                             cudaStream_t stream);
+
+}  // namespace pmfgpu

@@ -1,0 +1,290 @@
+// layout.cpp -- host construction of the device layouts (see layout.hpp).
+#include "layout.hpp"
+
+#include <algorithm>
+#include <atomic>
+#include <numeric>
+#include <stdexcept>
+#include <thread>
+
+namespace pmfgpu {
+
+void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn, int threads) {
+    if (n <= 0) return;
+    if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    threads = static_cast<int>(std::min<int64_t>(threads, std::max<int64_t>(1, n / 4096)));
+    if (threads <= 1) {
+        fn(0, n);
+        return;
+    }
+    std::vector<std::thread> ts;
+    ts.reserve(threads);
+    for (int t = 0; t < threads; ++t) {
+        const int64_t b = n * t / threads, e = n * (t + 1) / threads;
+        ts.emplace_back([&fn, b, e] { fn(b, e); });
+    }
+    for (auto& t : ts) t.join();
+}
+
+bool partition_balanced(const int64_t* costs, int32_t count, int p, int32_t* bounds) {
+    // runtime.hpp:91-136: binary search on the bottleneck, then a greedy packing sweep
+    if (p < 1) return false;
+    int64_t lo = 0, total = 0;
+    for (int32_t i = 0; i < count; ++i) {
+        if (costs[i] < 0) return false;
+        lo = std::max(lo, costs[i]);
+        total += costs[i];
+    }
+    auto blocks_needed = [&](int64_t budget) {
+        int blocks = 1;
+        int64_t cur = 0;
+        for (int32_t i = 0; i < count; ++i) {
+            if (cur + costs[i] > budget) {
+                ++blocks;
+                cur = costs[i];
+            } else {
+                cur += costs[i];
+            }
+        }
+        return blocks;
+    };
+    int64_t hi = total;
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (blocks_needed(mid) <= p) hi = mid;
+        else lo = mid + 1;
+    }
+    int nb = 0;
+    bounds[nb++] = 0;
+    int64_t cur = 0;
+    for (int32_t i = 0; i < count; ++i) {
+        if (cur + costs[i] > lo && nb <= p - 1) {
+            bounds[nb++] = i;
+            cur = costs[i];
+        } else {
+            cur += costs[i];
+        }
+    }
+    while (nb < p + 1) bounds[nb++] = count;
+    return true;
+}
+
+static inline int64_t round4(int64_t x) { return (x + 3) & ~int64_t(3); }
+
+SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const float* val,
+                               int32_t out_begin, int32_t out_end, const int32_t* gmap,
+                               int32_t gat_extent, int stage_arrays, int smem_budget_bytes,
+                               int ctas, bool allow_idx16) {
+    SweepLayout L;
+    const int32_t n_out = out_end - out_begin;
+    L.n_out = n_out;
+    L.gat_extent = gat_extent;
+    L.ctas = ctas;
+    auto gidx = [&](int64_t e) -> int32_t { return gmap ? gmap[idx[e]] : idx[e]; };
+
+    // ---- 1. gather panels ------------------------------------------------------------------
+    int64_t pg_cap = smem_budget_bytes / (4 * stage_arrays) - 1;
+    if (allow_idx16) pg_cap = std::min<int64_t>(pg_cap, 65535);
+    const int64_t nnz_side = start[out_end] - start[out_begin];
+    L.n_real = nnz_side;
+    if (gat_extent <= pg_cap) {
+        L.smem = true;
+        L.panel_size = std::max(gat_extent, 1);
+        L.n_panels = 1;
+        L.idx16 = allow_idx16 && gat_extent <= 65535;
+    } else {
+        const int32_t pg = static_cast<int32_t>(pg_cap);
+        const int32_t np = static_cast<int32_t>((static_cast<int64_t>(gat_extent) + pg - 1) / pg);
+        std::atomic<int64_t> segs{0};
+        parallel_for(n_out, [&](int64_t ob, int64_t oe) {
+            int64_t local = 0;
+            for (int64_t o = ob; o < oe; ++o) {
+                int32_t last = -1;
+                for (int64_t e = start[out_begin + o]; e < start[out_begin + o + 1]; ++e) {
+                    const int32_t p = gidx(e) / pg;
+                    if (p != last) {
+                        ++local;
+                        last = p;
+                    }
+                }
+            }
+            segs += local;
+        });
+        const double avg = segs.load() ? static_cast<double>(nnz_side) / segs.load() : 0.0;
+        if (avg >= 48.0) {
+            L.smem = true;
+            L.panel_size = pg;
+            L.n_panels = np;
+            L.idx16 = allow_idx16;
+        } else {
+            L.smem = false;
+            L.panel_size = gat_extent;
+            L.n_panels = 1;
+            L.idx16 = false;
+        }
+    }
+    L.sentinel = L.smem ? L.panel_size : gat_extent;
+    L.panel_base.resize(L.n_panels + 1);
+    for (int32_t p = 0; p < L.n_panels; ++p)
+        L.panel_base[p] = static_cast<int32_t>(static_cast<int64_t>(p) * L.panel_size);
+    L.panel_base[L.n_panels] = gat_extent;
+    const int32_t pg = L.panel_size;
+    const int32_t np = L.n_panels;
+
+    // ---- 2. segment lengths (panel-major) --------------------------------------------------
+    std::vector<int32_t> seg_len(static_cast<size_t>(np) * n_out, 0);
+    parallel_for(n_out, [&](int64_t ob, int64_t oe) {
+        for (int64_t o = ob; o < oe; ++o)
+            for (int64_t e = start[out_begin + o]; e < start[out_begin + o + 1]; ++e) {
+                const int32_t p = np == 1 ? 0 : gidx(e) / pg;
+                seg_len[static_cast<size_t>(p) * n_out + o]++;
+            }
+    });
+    std::vector<int64_t> seg_off(seg_len.size() + 1, 0);
+    int64_t nonempty = 0;
+    for (size_t s = 0; s < seg_len.size(); ++s) {
+        seg_off[s + 1] = seg_off[s] + round4(seg_len[s]);
+        nonempty += seg_len[s] > 0;
+    }
+    L.n_entries = seg_off.back();
+    L.avg_segment = nonempty ? static_cast<double>(nnz_side) / nonempty : 0.0;
+    if (L.n_entries >= (int64_t(1) << 32)) throw std::length_error("too many entries for 32-bit units");
+
+    // ---- 3. fill entries ---------------------------------------------------------------------
+    if (L.idx16) L.idx16v.assign(L.n_entries, static_cast<uint16_t>(L.sentinel));
+    else L.idx32v.assign(L.n_entries, L.sentinel);
+    L.val.assign(L.n_entries, 0.0f);
+    parallel_for(n_out, [&](int64_t ob, int64_t oe) {
+        for (int64_t o = ob; o < oe; ++o) {
+            int32_t cur_p = -1;
+            int64_t w = 0;
+            for (int64_t e = start[out_begin + o]; e < start[out_begin + o + 1]; ++e) {
+                const int32_t g = gidx(e);
+                const int32_t p = np == 1 ? 0 : g / pg;
+                if (p != cur_p) {
+                    cur_p = p;
+                    w = seg_off[static_cast<size_t>(p) * n_out + o];
+                }
+                const int32_t local = g - L.panel_base[p];
+                if (L.idx16) L.idx16v[w] = static_cast<uint16_t>(local);
+                else L.idx32v[w] = local;
+                L.val[w] = val[e];
+                ++w;
+            }
+        }
+    });
+
+    // ---- 4. units ----------------------------------------------------------------------------
+    std::vector<int32_t> cnt(n_out, 0);
+    for (int32_t p = 0; p < np; ++p)
+        for (int32_t o = 0; o < n_out; ++o) {
+            const size_t s = static_cast<size_t>(p) * n_out + o;
+            const int64_t real = seg_len[s];
+            if (real == 0) continue;
+            const int64_t padded = round4(real);
+            for (int64_t c = 0; c < padded; c += kUnitMax) {
+                const int64_t clen = std::min<int64_t>(kUnitMax, padded - c);
+                const int64_t creal = std::max<int64_t>(0, std::min<int64_t>(kUnitMax, real - c));
+                L.units.push_back(Unit{static_cast<uint32_t>(seg_off[s] + c),
+                                       static_cast<int32_t>(clen), o, -1});
+                L.unit_panel.push_back(p);
+                L.unit_real.push_back(static_cast<int32_t>(creal));
+                cnt[o]++;
+            }
+        }
+    std::vector<int32_t> slot_base(n_out, -1);
+    L.mo_start.push_back(0);
+    for (int32_t o = 0; o < n_out; ++o) {
+        if (cnt[o] == 1) continue;
+        slot_base[o] = L.mo_start.back();
+        L.mo_out.push_back(o);
+        L.mo_start.push_back(L.mo_start.back() + cnt[o]);
+    }
+    L.n_slots = L.mo_start.back();
+    {
+        std::vector<int32_t> run(n_out, 0);
+        for (auto& u : L.units)
+            if (slot_base[u.o] >= 0) u.slot = slot_base[u.o] + run[u.o]++;
+    }
+
+    // ---- 5. per-CTA pieces: contiguous unit ranges of equal cost, split at panel changes -----
+    const int64_t nu = static_cast<int64_t>(L.units.size());
+    std::vector<int64_t> pre(nu + 1, 0);
+    for (int64_t u = 0; u < nu; ++u) pre[u + 1] = pre[u] + L.units[u].len + kUnitOverhead;
+    L.piece_start.assign(ctas + 1, 0);
+    int64_t ub = 0;
+    for (int c = 0; c < ctas; ++c) {
+        const int64_t target = pre[nu] * (c + 1) / ctas;
+        int64_t ue = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
+        ue = std::max(ub, std::min(ue, nu));
+        if (c == ctas - 1) ue = nu;
+        for (int64_t u = ub; u < ue;) {
+            int64_t v = u;
+            while (v < ue && L.unit_panel[v] == L.unit_panel[u]) ++v;
+            L.pieces.push_back(Piece{L.unit_panel[u], static_cast<int32_t>(u),
+                                     static_cast<int32_t>(v), 0});
+            u = v;
+        }
+        L.piece_start[c + 1] = static_cast<int32_t>(L.pieces.size());
+        ub = ue;
+    }
+    return L;
+}
+
+void for_each_entry(const SweepLayout& L, const std::function<void(int32_t, int64_t, int64_t)>& fn) {
+    std::vector<int64_t> run(L.n_out, 0);
+    for (size_t u = 0; u < L.units.size(); ++u) {
+        const Unit& U = L.units[u];
+        for (int32_t x = 0; x < L.unit_real[u]; ++x)
+            fn(U.o, run[U.o] + x, static_cast<int64_t>(U.e0) + x);
+        run[U.o] += L.unit_real[u];
+    }
+}
+
+AlsLayout build_als_layout(const int64_t* start, const int32_t* idx, const float* val,
+                           int32_t out_begin, int32_t out_end, const int32_t* gmap, int chunk) {
+    AlsLayout L;
+    const int32_t n_out = out_end - out_begin;
+    L.n_out = n_out;
+    const int64_t base = start[out_begin];
+    L.n_entries = start[out_end] - base;
+    L.idx.resize(L.n_entries);
+    L.val.resize(L.n_entries);
+    parallel_for(L.n_entries, [&](int64_t b, int64_t e) {
+        for (int64_t x = b; x < e; ++x) {
+            L.idx[x] = gmap ? gmap[idx[base + x]] : idx[base + x];
+            L.val[x] = val[base + x];
+        }
+    });
+    std::vector<int32_t> cnt(n_out, 0);
+    for (int32_t o = 0; o < n_out; ++o) {
+        const int64_t b = start[out_begin + o] - base, e = start[out_begin + o + 1] - base;
+        if (b == e) {
+            L.empty_out.push_back(o);
+            continue;
+        }
+        for (int64_t c = b; c < e; c += chunk) {
+            L.units.push_back(Unit{static_cast<uint32_t>(c),
+                                   static_cast<int32_t>(std::min<int64_t>(chunk, e - c)), o, -1});
+            cnt[o]++;
+        }
+    }
+    std::vector<int32_t> slot_base(n_out, -1);
+    L.mo_start.push_back(0);
+    for (int32_t o = 0; o < n_out; ++o) {
+        if (cnt[o] <= 1) continue;
+        slot_base[o] = L.mo_start.back();
+        L.mo_out.push_back(o);
+        L.mo_start.push_back(L.mo_start.back() + cnt[o]);
+    }
+    L.n_slots = L.mo_start.back();
+    std::vector<int32_t> run(n_out, 0);
+    for (auto& u : L.units)
+        if (slot_base[u.o] >= 0) u.slot = slot_base[u.o] + run[u.o]++;
+    // longest units first: warps pull units from a global counter in this order (LPT balance)
+    std::stable_sort(L.units.begin(), L.units.end(),
+                     [](const Unit& a, const Unit& b) { return a.len > b.len; });
+    return L;
+}
+
+}  // namespace pmfgpu

@@ -1,0 +1,99 @@
+// layout.hpp -- host-side construction of the device data layouts (C++17, no CUDA).
+//
+// The reference keeps one CSR + one CSC of the ratings plus cross-links (sparse.hpp:64-216) and
+// walks them with per-row loops (ccd.hpp:153-197).  On the B200 each side of the matrix becomes a
+// "sweep layout": the entries of every output row (CSR side: users; CSC side: items) are grouped
+// by *gather panel* (a contiguous range of the opposing index whose factor values fit in shared
+// memory), each (panel, output) segment is padded to a multiple of 4 entries so a lane issues
+// 128-bit loads, and indices are stored panel-local (16-bit when the panel is <= 65535 wide).
+// Segments are cut into warp work units of at most kUnitMax entries; units of one output that
+// land in several panels / chunks produce partial (num, den) sums that a fixed-order finalize
+// combines, so every result is deterministic run to run.
+#pragma once
+
+#include <cstdint>
+#include <functional>
+#include <string>
+#include <vector>
+
+namespace pmfgpu {
+
+constexpr int kUnitMax = 4096;      // entries per warp work unit (multiple of 128)
+constexpr int kUnitOverhead = 96;   // cost model: fixed per-unit overhead in "entries"
+
+// 16-byte work unit, read with one 128-bit load.
+struct Unit {
+    uint32_t e0;   // first entry (multiple of 4 for sweep layouts)
+    int32_t len;   // entries (padded length for sweep layouts)
+    int32_t o;     // local output index
+    int32_t slot;  // -1: the only unit of its output (finalizes directly); else partial slot
+};
+
+struct Piece {   // a CTA's contiguous run of units inside one gather panel
+    int32_t panel;
+    int32_t ub, ue;
+    int32_t pad;
+};
+
+struct SweepLayout {
+    int32_t n_out = 0;        // outputs on this side (local)
+    int32_t gat_extent = 0;   // size of the gather index space (padded global space)
+    bool smem = true;         // gather vectors staged in shared memory per panel
+    bool idx16 = true;        // 16-bit panel-local indices
+    int32_t panel_size = 0;   // Pg; smem sentinel local index == Pg
+    int32_t n_panels = 0;
+    int32_t sentinel = 0;     // index value of padding entries
+    std::vector<int32_t> panel_base;  // n_panels + 1
+    int64_t n_entries = 0;            // padded entry count (multiple of 4)
+    int64_t n_real = 0;
+    std::vector<uint16_t> idx16v;
+    std::vector<int32_t> idx32v;
+    std::vector<float> val;           // padded values (A), padding = 0
+    std::vector<Unit> units;
+    std::vector<int32_t> unit_panel;
+    std::vector<int32_t> unit_real;   // real (unpadded) entries of each unit
+    std::vector<Piece> pieces;
+    std::vector<int32_t> piece_start; // ctas + 1
+    std::vector<int32_t> mo_out;      // outputs whose unit count != 1 (incl. empty outputs)
+    std::vector<int32_t> mo_start;    // size mo_out.size()+1, slot ranges
+    int32_t n_slots = 0;
+    int32_t ctas = 0;
+    double avg_segment = 0.0;
+};
+
+// Builds one side.  start/idx/val: the reference's CSR (or CSC) arrays restricted to outputs
+// [out_begin, out_end) (global offsets into idx/val).  gmap maps a global gather index to the
+// padded gather space (nullptr = identity); gat_extent is that space's size.  stage_arrays is the
+// number of gather vectors the promote sweep stages (2 on the CSR side, 3 on the CSC side).
+SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const float* val,
+                               int32_t out_begin, int32_t out_end, const int32_t* gmap,
+                               int32_t gat_extent, int stage_arrays, int smem_budget_bytes,
+                               int ctas, bool allow_idx16 = true);
+
+// Positions of the original entries of output o (in reference order) inside the padded layout:
+// calls fn(o, real_pos_in_output, padded_pos) for every real entry.
+void for_each_entry(const SweepLayout& L, const std::function<void(int32_t, int64_t, int64_t)>& fn);
+
+// ALS side: per-output chunks of at most `chunk` entries, unpadded, global (padded-space)
+// indices; balanced over `ctas` CTAs like the sweep layouts (no panels).
+struct AlsLayout {
+    int32_t n_out = 0;
+    int64_t n_entries = 0;
+    std::vector<int32_t> idx;
+    std::vector<float> val;
+    std::vector<Unit> units;         // slot -1: single-chunk output (solved in place)
+    std::vector<int32_t> mo_out, mo_start;
+    int32_t n_slots = 0;
+    std::vector<int32_t> empty_out;  // outputs with no entries (solve to 0, als.hpp:51-54)
+};
+
+AlsLayout build_als_layout(const int64_t* start, const int32_t* idx, const float* val,
+                           int32_t out_begin, int32_t out_end, const int32_t* gmap, int chunk);
+
+// runtime.hpp:91-136 partition_balanced (bounds p+1); returns false on invalid input.
+bool partition_balanced(const int64_t* costs, int32_t count, int p, int32_t* bounds);
+
+// Simple fork-join helper over [0, n) split into contiguous chunks.
+void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn, int threads = 0);
+
+}  // namespace pmfgpu

@@ -1,0 +1,1100 @@
+// pmf_gpu.cu -- C-ABI implementation: device contexts, CCD++ and ALS drivers, metrics, stage-level
+// entry points.  Mirrors the reference drivers ccdpp_train (ccd.hpp:349-404) and als_train
+// (als.hpp:188-233); the per-stage BSP barriers of the reference (runtime.hpp:177-203) become
+// kernel boundaries in one CUDA stream, and a whole CCD++ outer iteration is captured once as a
+// CUDA graph.  Multi-GPU contexts own a CSR row block and a CSC column block (runtime.hpp:91-136)
+// and all-gather u / v (CCD++) or W / H blocks (ALS) over NCCL.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/pmf_gpu.h"
+#include "device.hpp"
+#include "layout.hpp"
+
+namespace pmfgpu {
+
+thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+struct PmfError : std::runtime_error {
+    pmf_status st;
+    PmfError(pmf_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define CUDA_TRY(x)                                                                                  \
+    do {                                                                                             \
+        cudaError_t e_ = (x);                                                                        \
+        if (e_ != cudaSuccess)                                                                       \
+            throw PmfError(PMF_RUNTIME_ERROR, std::string("CUDA error: ") + cudaGetErrorString(e_) + \
+                                                  " at " #x);                                        \
+    } while (0)
+
+#define NCCL_TRY(x)                                                                                  \
+    do {                                                                                             \
+        ncclResult_t r_ = (x);                                                                       \
+        if (r_ != ncclSuccess)                                                                       \
+            throw PmfError(PMF_RUNTIME_ERROR, std::string("NCCL error: ") + ncclGetErrorString(r_) + \
+                                                  " at " #x);                                        \
+    } while (0)
+
+template <class F>
+pmf_status guard(F&& f) {
+    try {
+        f();
+        return PMF_OK;
+    } catch (const PmfError& e) {
+        g_err = e.what();
+        return e.st;
+    } catch (const std::bad_alloc&) {
+        g_err = "host out of memory";
+        return PMF_RUNTIME_ERROR;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return PMF_RUNTIME_ERROR;
+    }
+}
+
+[[noreturn]] void invalid(const std::string& m) { throw PmfError(PMF_INVALID_ARGUMENT, m); }
+
+constexpr int kSmemBudget = 220 * 1024;
+
+// ---- device memory -----------------------------------------------------------------------------
+struct DevMem {
+    std::vector<void*> blocks;
+    template <class T>
+    T* alloc(size_t count, bool zero = true) {
+        void* p = nullptr;
+        if (count == 0) count = 1;
+        CUDA_TRY(cudaMalloc(&p, count * sizeof(T)));
+        blocks.push_back(p);
+        if (zero) CUDA_TRY(cudaMemset(p, 0, count * sizeof(T)));
+        return static_cast<T*>(p);
+    }
+    template <class T>
+    T* upload(const std::vector<T>& v, cudaStream_t s, int64_t* h2d) {
+        T* p = alloc<T>(v.size(), false);
+        if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (h2d) *h2d += static_cast<int64_t>(v.size() * sizeof(T));
+        return p;
+    }
+    void free_all() {
+        for (void* p : blocks) cudaFree(p);
+        blocks.clear();
+    }
+    ~DevMem() { free_all(); }
+};
+
+struct Ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    int32_t m = 0, n = 0;
+    int64_t nnz = 0;
+    // distribution
+    int rank = 0, world = 1;
+    ncclComm_t comm = nullptr;
+    int32_t row_begin = 0, row_end = 0, col_begin = 0, col_end = 0;
+    int32_t Bm = 0, Bn = 0, ext_m = 0, ext_n = 0, ldm = 0, ldn = 0;
+    std::vector<int32_t> rmap, cmap;  // global -> padded (empty = identity)
+    int64_t local_nnz_csr = 0, local_nnz_csc = 0;
+    // host metadata kept for residual readback
+    SweepLayout hcsr, hcsc;  // value/index arrays released after upload
+    std::vector<int64_t> row_start_local, col_start_local;
+    DevMem mem;
+    DevSweep csr, csc;
+    float* A_csr = nullptr;   // immutable ratings, padded CSR layout (objective reads A, not R)
+    float* A_csc = nullptr;
+    // CCD++ model
+    int mode = 0;  // 0 none, 1 ccdpp, 2 als
+    int k = 0;
+    float lambda = 0.f;
+    int inner = 0;
+    DevMem model_mem;
+    float* W = nullptr;  // CCD++: column-major k x ldm ; ALS: row-major ext_m x k
+    float* H = nullptr;
+    float* ubuf = nullptr;
+    float* vbuf = nullptr;
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t graph_exec = nullptr;
+    int64_t launches_per_iter = 0;
+    bool profiling = false;
+    double stat_u_ms = 0, stat_v_ms = 0;
+    int64_t stat_u_n = 0, stat_v_n = 0;
+    // ALS
+    bool als_built = false;
+    DevMem als_mem;
+    DevAls als_csr, als_csc;
+    int* d_counter = nullptr;
+    int* d_status = nullptr;
+    bool als_weighted = false;
+    // eval
+    DevMem eval_mem;
+    double* unit_loss = nullptr;
+    double* red_scratch = nullptr;
+    double* red_out = nullptr;  // [0] loss, [1] reg W, [2] reg H, [3] probe sse
+    DevTriplet* probe = nullptr;
+    int64_t n_probe = 0;
+    DevMem probe_mem;
+    int64_t h2d = 0, d2h = 0;
+    double setup_seconds = 0;
+
+    ~Ctx() {
+        if (graph_exec) cudaGraphExecDestroy(graph_exec);
+        if (graph) cudaGraphDestroy(graph);
+        if (comm) ncclCommDestroy(comm);
+        if (stream) cudaStreamDestroy(stream);
+    }
+    int32_t prow(int32_t i) const { return rmap.empty() ? i : rmap[i]; }
+    int32_t pcol(int32_t j) const { return cmap.empty() ? j : cmap[j]; }
+};
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+void check_view(const pmf_matrix_view* a) {
+    if (!a) invalid("matrix view is null");
+    if (a->m < 0 || a->n < 0) invalid("matrix dimensions must be non-negative");
+    if (a->nnz < 0) invalid("nnz must be non-negative");
+    if (!a->row_start || !a->col_start) invalid("matrix offsets are null");
+    if (a->nnz > 0 && (!a->col_of || !a->val_row || !a->row_of || !a->val_col)) invalid("matrix arrays are null");
+    if (a->row_start[0] != 0 || a->row_start[a->m] != a->nnz || a->col_start[0] != 0 || a->col_start[a->n] != a->nnz)
+        throw PmfError(PMF_DATA_ERROR, "matrix offsets inconsistent with nnz");
+}
+
+void ensure_device() {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+        cudaGetLastError();
+        throw PmfError(PMF_RUNTIME_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
+    }
+}
+
+DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
+    DevSweep D;
+    D.n_out = L.n_out;
+    D.gat_extent = L.gat_extent;
+    D.panel_size = L.panel_size;
+    D.n_panels = L.n_panels;
+    D.sentinel = L.sentinel;
+    D.smem = L.smem;
+    D.idx16 = L.idx16;
+    D.n_entries = L.n_entries;
+    D.n_units = static_cast<int32_t>(L.units.size());
+    D.n_mo = static_cast<int32_t>(L.mo_out.size());
+    D.ctas = L.ctas;
+    D.n_slots = L.n_slots;
+    if (L.idx16) D.idx = c.mem.upload(L.idx16v, c.stream, &c.h2d);
+    else D.idx = c.mem.upload(L.idx32v, c.stream, &c.h2d);
+    D.R = c.mem.alloc<float>(L.n_entries + 4, false);
+    float* A = c.mem.upload(L.val, c.stream, &c.h2d);
+    CUDA_TRY(cudaMemcpyAsync(D.R, A, L.val.size() * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+    *A_copy = A;
+    D.units = c.mem.upload(L.units, c.stream, &c.h2d);
+    D.unit_panel = c.mem.upload(L.unit_panel, c.stream, &c.h2d);
+    D.pieces = c.mem.upload(L.pieces, c.stream, &c.h2d);
+    D.piece_start = c.mem.upload(L.piece_start, c.stream, &c.h2d);
+    D.panel_base = c.mem.upload(L.panel_base, c.stream, &c.h2d);
+    D.mo_out = c.mem.upload(L.mo_out, c.stream, &c.h2d);
+    D.mo_start = c.mem.upload(L.mo_start, c.stream, &c.h2d);
+    D.partial = c.mem.alloc<float2>(std::max(1, L.n_slots));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    // keep only the metadata needed for residual readback
+    std::vector<uint16_t>().swap(L.idx16v);
+    std::vector<int32_t>().swap(L.idx32v);
+    std::vector<float>().swap(L.val);
+    return D;
+}
+
+std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, int world, const uint8_t* id) {
+    check_view(a);
+    ensure_device();
+    const double t0 = now_s();
+    auto c = std::make_unique<Ctx>();
+    if (device < 0) CUDA_TRY(cudaGetDevice(&device));
+    c->device = device;
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    c->m = a->m;
+    c->n = a->n;
+    c->nnz = a->nnz;
+    c->rank = rank;
+    c->world = world;
+    if (world > 1) {
+        ncclUniqueId uid;
+        std::memcpy(&uid, id, sizeof(uid));
+        NCCL_TRY(ncclCommInitRank(&c->comm, world, uid, rank));
+    }
+    // row / column blocks (runtime.hpp:73-136, 4|Omega| costs)
+    std::vector<int32_t> rb(world + 1), cbd(world + 1);
+    {
+        std::vector<int64_t> rc(a->m), cc(a->n);
+        for (int32_t i = 0; i < a->m; ++i) rc[i] = 4 * (a->row_start[i + 1] - a->row_start[i]);
+        for (int32_t j = 0; j < a->n; ++j) cc[j] = 4 * (a->col_start[j + 1] - a->col_start[j]);
+        partition_balanced(rc.data(), a->m, world, rb.data());
+        partition_balanced(cc.data(), a->n, world, cbd.data());
+    }
+    c->row_begin = rb[rank];
+    c->row_end = rb[rank + 1];
+    c->col_begin = cbd[rank];
+    c->col_end = cbd[rank + 1];
+    int32_t bm = 0, bn = 0;
+    for (int r = 0; r < world; ++r) {
+        bm = std::max(bm, rb[r + 1] - rb[r]);
+        bn = std::max(bn, cbd[r + 1] - cbd[r]);
+    }
+    c->Bm = world == 1 ? a->m : bm;
+    c->Bn = world == 1 ? a->n : bn;
+    c->ext_m = world * c->Bm;
+    c->ext_n = world * c->Bn;
+    c->ldm = ((c->ext_m + 1 + 31) / 32) * 32;
+    c->ldn = ((c->ext_n + 1 + 31) / 32) * 32;
+    if (world > 1) {
+        c->rmap.resize(a->m);
+        c->cmap.resize(a->n);
+        for (int r = 0; r < world; ++r) {
+            for (int32_t i = rb[r]; i < rb[r + 1]; ++i) c->rmap[i] = r * c->Bm + (i - rb[r]);
+            for (int32_t j = cbd[r]; j < cbd[r + 1]; ++j) c->cmap[j] = r * c->Bn + (j - cbd[r]);
+        }
+    }
+    const int32_t* rmap = c->rmap.empty() ? nullptr : c->rmap.data();
+    const int32_t* cmap = c->cmap.empty() ? nullptr : c->cmap.data();
+    c->hcsr = build_sweep_layout(a->row_start, a->col_of, a->val_row, c->row_begin, c->row_end, cmap, c->ext_n,
+                                 2, kSmemBudget, c->sm_count);
+    c->hcsc = build_sweep_layout(a->col_start, a->row_of, a->val_col, c->col_begin, c->col_end, rmap, c->ext_m,
+                                 3, kSmemBudget, c->sm_count);
+    c->local_nnz_csr = a->row_start[c->row_end] - a->row_start[c->row_begin];
+    c->local_nnz_csc = a->col_start[c->col_end] - a->col_start[c->col_begin];
+    c->row_start_local.assign(a->row_start + c->row_begin, a->row_start + c->row_end + 1);
+    c->col_start_local.assign(a->col_start + c->col_begin, a->col_start + c->col_end + 1);
+    static bool attrs_set = false;
+    if (!attrs_set) {
+        sweep_set_attributes(kSmemBudget + 1024);
+        als_set_attributes();
+        attrs_set = true;
+    }
+    c->csr = upload_sweep(*c, c->hcsr, &c->A_csr);
+    c->csc = upload_sweep(*c, c->hcsc, &c->A_csc);
+    // eval scratch
+    c->unit_loss = c->eval_mem.alloc<double>(std::max(c->csr.n_units, 1));
+    c->red_scratch = c->eval_mem.alloc<double>(4096);
+    c->red_out = c->eval_mem.alloc<double>(8);
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->setup_seconds = now_s() - t0;
+    return c;
+}
+
+// ---- CCD++ --------------------------------------------------------------------------------------
+
+void reset_graph(Ctx& c) {
+    if (c.graph_exec) cudaGraphExecDestroy(c.graph_exec);
+    if (c.graph) cudaGraphDestroy(c.graph);
+    c.graph_exec = nullptr;
+    c.graph = nullptr;
+}
+
+void alloc_ccd_model(Ctx& c, int k) {
+    reset_graph(c);
+    c.model_mem.free_all();
+    c.W = c.model_mem.alloc<float>(static_cast<size_t>(k) * c.ldm);
+    c.H = c.model_mem.alloc<float>(static_cast<size_t>(k) * c.ldn);
+    c.ubuf = c.model_mem.alloc<float>(c.ldm);
+    c.vbuf = c.model_mem.alloc<float>(c.ldn);
+    c.k = k;
+}
+
+// model.hpp:86-93 init_random_items on the host (mt19937, bit-exact), returned row-major n x k
+std::vector<float> init_items_host(int32_t n, int k, uint64_t seed) {
+    std::vector<float> H(static_cast<size_t>(n) * k);
+    std::mt19937 gen(static_cast<std::mt19937::result_type>(seed));
+    const double scale = 1.0 / std::sqrt(static_cast<double>(k));
+    for (auto& x : H) x = static_cast<float>(((static_cast<double>(gen()) + 1.0) * (1.0 / 4294967296.0)) * scale);
+    return H;
+}
+
+void upload_colmajor(Ctx& c, float* dst, int64_t ld, const float* rowmajor, int32_t count, int k, bool rows) {
+    std::vector<float> tmp(static_cast<size_t>(k) * ld, 0.f);
+    for (int32_t i = 0; i < count; ++i) {
+        const int32_t p = rows ? c.prow(i) : c.pcol(i);
+        for (int t = 0; t < k; ++t) tmp[static_cast<size_t>(t) * ld + p] = rowmajor[static_cast<size_t>(i) * k + t];
+    }
+    CUDA_TRY(cudaMemcpyAsync(dst, tmp.data(), tmp.size() * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    c.h2d += static_cast<int64_t>(tmp.size() * sizeof(float));
+}
+
+void upload_rowmajor(Ctx& c, float* dst, int32_t ext, const float* rowmajor, int32_t count, int k, bool rows) {
+    std::vector<float> tmp(static_cast<size_t>(ext) * k, 0.f);
+    for (int32_t i = 0; i < count; ++i) {
+        const int32_t p = rows ? c.prow(i) : c.pcol(i);
+        std::memcpy(&tmp[static_cast<size_t>(p) * k], rowmajor + static_cast<size_t>(i) * k, sizeof(float) * k);
+    }
+    CUDA_TRY(cudaMemcpyAsync(dst, tmp.data(), tmp.size() * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    c.h2d += static_cast<int64_t>(tmp.size() * sizeof(float));
+}
+
+void reset_residual(Ctx& c) {
+    CUDA_TRY(cudaMemcpyAsync(c.csr.R, c.A_csr, c.csr.n_entries * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+    CUDA_TRY(cudaMemcpyAsync(c.csc.R, c.A_csc, c.csc.n_entries * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+}
+
+void allgather(Ctx& c, float* buf, int64_t block) {
+    if (c.world > 1)
+        NCCL_TRY(ncclAllGather(buf + static_cast<int64_t>(c.rank) * block, buf, block, ncclFloat, c.comm, c.stream));
+}
+
+struct SweepTimer {
+    Ctx& c;
+    cudaEvent_t a = nullptr, b = nullptr;
+    bool on;
+    explicit SweepTimer(Ctx& cc) : c(cc), on(cc.profiling) {
+        if (on) {
+            cudaEventCreate(&a);
+            cudaEventCreate(&b);
+        }
+    }
+    ~SweepTimer() {
+        if (a) cudaEventDestroy(a);
+        if (b) cudaEventDestroy(b);
+    }
+    void start() {
+        if (on) cudaEventRecord(a, c.stream);
+    }
+    void stop(bool u) {
+        if (!on) return;
+        cudaEventRecord(b, c.stream);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        if (u) {
+            c.stat_u_ms += ms;
+            c.stat_u_n++;
+        } else {
+            c.stat_v_ms += ms;
+            c.stat_v_n++;
+        }
+    }
+};
+
+// Enqueues one CCD++ outer iteration (ccd.hpp:373-393) on c.stream; returns kernels launched.
+int64_t enqueue_ccd_iteration(Ctx& c) {
+    int64_t launched = 0;
+    const int k = c.k;
+    SweepTimer tm(c);
+    for (int t = 0; t < k; ++t) {
+        const int tp = (t + k - 1) % k;
+        float* Wt = c.W + static_cast<int64_t>(t) * c.ldm;
+        float* Wp = c.W + static_cast<int64_t>(tp) * c.ldm;
+        float* Ht = c.H + static_cast<int64_t>(t) * c.ldn;
+        float* Hp = c.H + static_cast<int64_t>(tp) * c.ldn;
+        for (int s = 0; s < c.inner; ++s) {
+            SweepOperands ou;
+            ou.lambda = c.lambda;
+            ou.out = c.ubuf;
+            ou.out_off = c.rank * c.Bm;
+            if (s == 0) {
+                ou.ga = Hp;  // v'
+                ou.gb = Ht;  // h (also the v of the first u update)
+                ou.gn = Ht;
+                ou.oa = Wp;  // u'
+                ou.ob = Wt;  // w
+            } else {
+                ou.gn = c.vbuf;
+            }
+            tm.start();
+            launched += launch_sweep(c.csr, s == 0 ? kPromote : kPlain, true, ou, c.stream);
+            tm.stop(true);
+            allgather(c, c.ubuf, c.Bm);
+            SweepOperands ov;
+            ov.lambda = c.lambda;
+            ov.out = c.vbuf;
+            ov.out_off = c.rank * c.Bn;
+            ov.gn = c.ubuf;
+            if (s == 0) {
+                ov.ga = Wp;  // u'
+                ov.gb = Wt;  // w
+                ov.oa = Hp;  // v'
+                ov.ob = Ht;  // h
+            }
+            tm.start();
+            launched += launch_sweep(c.csc, s == 0 ? kPromote : kPlain, false, ov, c.stream);
+            tm.stop(false);
+            allgather(c, c.vbuf, c.Bn);
+        }
+        // writeback of the column pair (ccd.hpp:209, :226); the residual part is deferred
+        CUDA_TRY(cudaMemcpyAsync(Wt, c.ubuf, sizeof(float) * c.ext_m, cudaMemcpyDeviceToDevice, c.stream));
+        CUDA_TRY(cudaMemcpyAsync(Ht, c.vbuf, sizeof(float) * c.ext_n, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    CUDA_TRY(cudaGetLastError());
+    return launched;
+}
+
+void ccd_begin(Ctx& c, const pmf_ccd_config* cfg) {
+    if (!cfg) invalid("config is null");
+    // ccd.hpp:43-49
+    if (cfg->k < 1) invalid("k must be >= 1");
+    if (cfg->lambda < 0.f) invalid("lambda must be >= 0");
+    if (cfg->outer_iters < 1) invalid("outer_iters must be >= 1");
+    if (cfg->inner_iters < 1) invalid("inner_iters must be >= 1");
+    CUDA_TRY(cudaSetDevice(c.device));
+    alloc_ccd_model(c, cfg->k);
+    c.mode = 1;
+    c.lambda = cfg->lambda;
+    c.inner = cfg->inner_iters;
+    const auto H = init_items_host(c.n, cfg->k, cfg->seed);
+    upload_colmajor(c, c.H, c.ldn, H.data(), c.n, cfg->k, false);
+    reset_residual(c);
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+}
+
+void ccd_iterate(Ctx& c, int n_outer, double* secs) {
+    if (c.mode != 1) invalid("ccdpp_begin has not been called");
+    CUDA_TRY(cudaSetDevice(c.device));
+    if (c.profiling) {
+        reset_graph(c);
+        c.stat_u_ms = c.stat_v_ms = 0;
+        c.stat_u_n = c.stat_v_n = 0;
+    } else if (!c.graph_exec) {
+        CUDA_TRY(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
+        int64_t launched = 0;
+        try {
+            launched = enqueue_ccd_iteration(c);
+        } catch (...) {
+            cudaGraph_t g;
+            cudaStreamEndCapture(c.stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        CUDA_TRY(cudaStreamEndCapture(c.stream, &c.graph));
+        CUDA_TRY(cudaGraphInstantiate(&c.graph_exec, c.graph, 0));
+        c.launches_per_iter = launched;
+    }
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    for (int it = 0; it < n_outer; ++it) {
+        CUDA_TRY(cudaEventRecord(e0, c.stream));
+        if (c.profiling) c.launches_per_iter = enqueue_ccd_iteration(c);
+        else CUDA_TRY(cudaGraphLaunch(c.graph_exec, c.stream));
+        CUDA_TRY(cudaEventRecord(e1, c.stream));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        if (secs) secs[it] = ms * 1e-3;
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CUDA_TRY(cudaGetLastError());
+}
+
+// ---- ALS ----------------------------------------------------------------------------------------
+
+DevAls upload_als(Ctx& c, const AlsLayout& L, int k) {
+    DevAls D;
+    D.n_out = L.n_out;
+    D.n_units = static_cast<int32_t>(L.units.size());
+    D.n_mo = static_cast<int32_t>(L.mo_out.size());
+    D.n_slots = L.n_slots;
+    D.n_empty = static_cast<int32_t>(L.empty_out.size());
+    D.n_entries = L.n_entries;
+    D.idx = c.als_mem.upload(L.idx, c.stream, &c.h2d);
+    D.val = c.als_mem.upload(L.val, c.stream, &c.h2d);
+    D.units = c.als_mem.upload(L.units, c.stream, &c.h2d);
+    D.mo_out = c.als_mem.upload(L.mo_out, c.stream, &c.h2d);
+    D.mo_start = c.als_mem.upload(L.mo_start, c.stream, &c.h2d);
+    D.empty_out = c.als_mem.upload(L.empty_out, c.stream, &c.h2d);
+    D.partial = nullptr;
+    (void)k;
+    return D;
+}
+
+// ALS layouts need the host matrix: built during ctx creation when requested.
+struct AlsHost {
+    AlsLayout csr, csc;
+};
+
+constexpr int kAlsChunk = 4096;
+
+void build_als(Ctx& c, const pmf_matrix_view* a) {
+    if (c.als_built) return;
+    const int32_t* rmap = c.rmap.empty() ? nullptr : c.rmap.data();
+    const int32_t* cmap = c.cmap.empty() ? nullptr : c.cmap.data();
+    AlsLayout lc = build_als_layout(a->row_start, a->col_of, a->val_row, c.row_begin, c.row_end, cmap, kAlsChunk);
+    AlsLayout lr = build_als_layout(a->col_start, a->row_of, a->val_col, c.col_begin, c.col_end, rmap, kAlsChunk);
+    c.als_csr = upload_als(c, lc, 0);
+    c.als_csc = upload_als(c, lr, 0);
+    c.d_counter = c.als_mem.alloc<int>(4);
+    c.d_status = c.als_mem.alloc<int>(4);
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    c.als_built = true;
+}
+
+void als_alloc_partials(Ctx& c, int k) {
+    // partial buffers depend on k; (re)allocate in model_mem
+    const int64_t stride = static_cast<int64_t>(k) * k + k + 1;
+    c.als_csr.partial = c.model_mem.alloc<float>(std::max<int64_t>(1, c.als_csr.n_slots * stride), false);
+    c.als_csc.partial = c.model_mem.alloc<float>(std::max<int64_t>(1, c.als_csc.n_slots * stride), false);
+}
+
+void als_begin(Ctx& c, const pmf_als_config* cfg) {
+    if (!cfg) invalid("config is null");
+    // als.hpp:34-39
+    if (cfg->k < 1) invalid("k must be >= 1");
+    if (!(cfg->lambda > 0.f)) invalid("als requires lambda > 0");
+    if (cfg->outer_iters < 1) invalid("outer_iters must be >= 1");
+    if (cfg->k > 64) invalid("the B200 ALS kernels support k <= 64");
+    if (!c.als_built) invalid("context was created without ALS layouts");
+    CUDA_TRY(cudaSetDevice(c.device));
+    reset_graph(c);
+    c.model_mem.free_all();
+    c.k = cfg->k;
+    c.lambda = cfg->lambda;
+    c.als_weighted = (cfg->flags & PMF_ALS_WEIGHTED_LAMBDA) != 0;
+    c.W = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_m + 1) * c.k);
+    c.H = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_n + 1) * c.k);
+    als_alloc_partials(c, c.k);
+    const auto H = init_items_host(c.n, cfg->k, cfg->seed);
+    upload_rowmajor(c, c.H, c.ext_n, H.data(), c.n, cfg->k, false);
+    c.mode = 2;
+}
+
+int64_t enqueue_als_iteration(Ctx& c) {
+    int64_t launched = 0;
+    // W phase from the old H, then H phase from the new W (als.hpp:176-184)
+    launched += launch_als_half(c.als_csr, c.H, c.W, c.rank * c.Bm, c.k, c.lambda, c.als_weighted, c.d_counter,
+                                c.d_status, c.sm_count, c.stream);
+    allgather(c, c.W, static_cast<int64_t>(c.Bm) * c.k);
+    launched += launch_als_half(c.als_csc, c.W, c.H, c.rank * c.Bn, c.k, c.lambda, c.als_weighted, c.d_counter + 1,
+                                c.d_status, c.sm_count, c.stream);
+    allgather(c, c.H, static_cast<int64_t>(c.Bn) * c.k);
+    return launched;
+}
+
+void als_iterate(Ctx& c, int n_outer, double* secs) {
+    if (c.mode != 2) invalid("als_begin has not been called");
+    CUDA_TRY(cudaSetDevice(c.device));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    for (int it = 0; it < n_outer; ++it) {
+        CUDA_TRY(cudaMemsetAsync(c.d_status, 0, sizeof(int), c.stream));
+        CUDA_TRY(cudaEventRecord(e0, c.stream));
+        c.launches_per_iter = enqueue_als_iteration(c);
+        CUDA_TRY(cudaEventRecord(e1, c.stream));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        if (secs) secs[it] = ms * 1e-3;
+        int st = 0;
+        CUDA_TRY(cudaMemcpy(&st, c.d_status, sizeof(int), cudaMemcpyDeviceToHost));
+        if (st == 4) throw PmfError(PMF_NOT_POSITIVE_DEFINITE, "non-positive pivot in an ALS row solve");
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CUDA_TRY(cudaGetLastError());
+}
+
+// ---- metrics ------------------------------------------------------------------------------------
+
+FactorView wview(const Ctx& c) {
+    if (c.mode == 1) return FactorView{c.W, 1, c.ldm};
+    return FactorView{c.W, c.k, 1};
+}
+FactorView hview(const Ctx& c) {
+    if (c.mode == 1) return FactorView{c.H, 1, c.ldn};
+    return FactorView{c.H, c.k, 1};
+}
+
+void metrics(Ctx& c, double* objective, double* rmse, double* train_rmse) {
+    if (c.mode == 0) invalid("no model: call ccdpp_begin or als_begin first");
+    CUDA_TRY(cudaSetDevice(c.device));
+    const FactorView W = wview(c), H = hview(c);
+    launch_unit_loss(c.csr, c.A_csr, c.rank * c.Bm, W, H, c.k, c.unit_loss, c.stream);
+    launch_sum(c.unit_loss, c.csr.n_units, c.red_scratch, c.red_out + 0, c.stream);
+    const int64_t wn = c.mode == 1 ? static_cast<int64_t>(c.k) * c.ldm : static_cast<int64_t>(c.ext_m + 1) * c.k;
+    const int64_t hn = c.mode == 1 ? static_cast<int64_t>(c.k) * c.ldn : static_cast<int64_t>(c.ext_n + 1) * c.k;
+    launch_sumsq(c.W, wn, c.red_scratch + 1024, c.red_out + 1, c.stream);
+    launch_sumsq(c.H, hn, c.red_scratch + 2048, c.red_out + 2, c.stream);
+    if (c.n_probe > 0) launch_probe_sse(c.probe, c.n_probe, W, H, c.k, c.red_scratch + 3072, c.red_out + 3, c.stream);
+    if (c.world > 1) NCCL_TRY(ncclAllReduce(c.red_out, c.red_out, 1, ncclDouble, ncclSum, c.comm, c.stream));
+    double h[4] = {0, 0, 0, 0};
+    CUDA_TRY(cudaMemcpyAsync(h, c.red_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    const double lam = static_cast<double>(c.lambda);  // Real lambda widened (ccd.hpp:394)
+    if (objective) *objective = h[0] + lam * (h[1] + h[2]);
+    if (train_rmse) *train_rmse = c.nnz > 0 ? std::sqrt(h[0] / static_cast<double>(c.nnz)) : 0.0;
+    if (rmse) *rmse = c.n_probe > 0 ? std::sqrt(h[3] / static_cast<double>(c.n_probe)) : std::nan("");
+}
+
+void set_probe(Ctx& c, const pmf_triplet* probe, int64_t n) {
+    if (n < 0 || (n > 0 && !probe)) invalid("probe is null");
+    for (int64_t x = 0; x < n; ++x)
+        if (probe[x].user < 0 || probe[x].user >= c.m || probe[x].item < 0 || probe[x].item >= c.n)
+            invalid("probe index outside training dimensions");  // ccd.hpp:298-303
+    CUDA_TRY(cudaSetDevice(c.device));
+    c.probe_mem.free_all();
+    c.probe = nullptr;
+    c.n_probe = n;
+    if (n == 0) return;
+    std::vector<DevTriplet> t(n);
+    for (int64_t x = 0; x < n; ++x) t[x] = DevTriplet{c.prow(probe[x].user), c.pcol(probe[x].item), probe[x].rating};
+    c.probe = c.probe_mem.upload(t, c.stream, &c.h2d);
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+}
+
+void get_model(Ctx& c, float* W, float* H) {
+    if (c.mode == 0) invalid("no model");
+    CUDA_TRY(cudaSetDevice(c.device));
+    const int k = c.k;
+    if (c.mode == 1) {
+        std::vector<float> w(static_cast<size_t>(k) * c.ldm), h(static_cast<size_t>(k) * c.ldn);
+        CUDA_TRY(cudaMemcpy(w.data(), c.W, w.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(h.data(), c.H, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        c.d2h += static_cast<int64_t>((w.size() + h.size()) * sizeof(float));
+        if (W)
+            for (int32_t i = 0; i < c.m; ++i)
+                for (int t = 0; t < k; ++t) W[static_cast<size_t>(i) * k + t] = w[static_cast<size_t>(t) * c.ldm + c.prow(i)];
+        if (H)
+            for (int32_t j = 0; j < c.n; ++j)
+                for (int t = 0; t < k; ++t) H[static_cast<size_t>(j) * k + t] = h[static_cast<size_t>(t) * c.ldn + c.pcol(j)];
+    } else {
+        std::vector<float> w(static_cast<size_t>(c.ext_m) * k), h(static_cast<size_t>(c.ext_n) * k);
+        CUDA_TRY(cudaMemcpy(w.data(), c.W, w.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(h.data(), c.H, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        c.d2h += static_cast<int64_t>((w.size() + h.size()) * sizeof(float));
+        if (W)
+            for (int32_t i = 0; i < c.m; ++i)
+                std::memcpy(W + static_cast<size_t>(i) * k, &w[static_cast<size_t>(c.prow(i)) * k], sizeof(float) * k);
+        if (H)
+            for (int32_t j = 0; j < c.n; ++j)
+                std::memcpy(H + static_cast<size_t>(j) * k, &h[static_cast<size_t>(c.pcol(j)) * k], sizeof(float) * k);
+    }
+}
+
+void set_model(Ctx& c, const float* W, const float* H, int k) {
+    if (c.mode == 0) invalid("no model: call ccdpp_begin or als_begin first");
+    if (k != c.k) invalid("rank does not match the active model");
+    if (c.mode == 1) {
+        upload_colmajor(c, c.W, c.ldm, W, c.m, k, true);
+        upload_colmajor(c, c.H, c.ldn, H, c.n, k, false);
+    } else {
+        upload_rowmajor(c, c.W, c.ext_m, W, c.m, k, true);
+        upload_rowmajor(c, c.H, c.ext_n, H, c.n, k, false);
+    }
+}
+
+// host scatter/gather between reference order and the padded layout
+void put_values(Ctx& c, const SweepLayout& L, float* dst, const float* src, const std::vector<int64_t>& start) {
+    std::vector<float> tmp(L.n_entries, 0.f);
+    const int64_t base = start[0];
+    for_each_entry(L, [&](int32_t o, int64_t r, int64_t p) { tmp[p] = src[start[o] - base + r]; });
+    CUDA_TRY(cudaMemcpyAsync(dst, tmp.data(), tmp.size() * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+}
+
+void get_values(Ctx& c, const SweepLayout& L, const float* src, float* dst, const std::vector<int64_t>& start) {
+    std::vector<float> tmp(L.n_entries);
+    CUDA_TRY(cudaMemcpy(tmp.data(), src, tmp.size() * sizeof(float), cudaMemcpyDeviceToHost));
+    const int64_t base = start[0];
+    for_each_entry(L, [&](int32_t o, int64_t r, int64_t p) { dst[start[o] - base + r] = tmp[p]; });
+}
+
+void get_residual(Ctx& c, float* r_row, float* r_col) {
+    if (c.mode != 1) invalid("no CCD++ state");
+    if (c.world > 1) invalid("residual readback is single-GPU only");
+    CUDA_TRY(cudaSetDevice(c.device));
+    // apply the deferred writeback of the last step (t = k-1) on copies
+    const int tp = c.k - 1;
+    DevMem tmp;
+    DevSweep r = c.csr, q = c.csc;
+    r.R = tmp.alloc<float>(c.csr.n_entries + 4, false);
+    q.R = tmp.alloc<float>(c.csc.n_entries + 4, false);
+    CUDA_TRY(cudaMemcpyAsync(r.R, c.csr.R, c.csr.n_entries * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+    CUDA_TRY(cudaMemcpyAsync(q.R, c.csc.R, c.csc.n_entries * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+    SweepOperands o1;
+    o1.oa = c.W + static_cast<int64_t>(tp) * c.ldm;
+    o1.ga = c.H + static_cast<int64_t>(tp) * c.ldn;
+    launch_sweep(r, kDemote, true, o1, c.stream);
+    SweepOperands o2;
+    o2.oa = c.H + static_cast<int64_t>(tp) * c.ldn;
+    o2.ga = c.W + static_cast<int64_t>(tp) * c.ldm;
+    launch_sweep(q, kDemote, false, o2, c.stream);
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (r_row) get_values(c, c.hcsr, r.R, r_row, c.row_start_local);
+    if (r_col) get_values(c, c.hcsc, q.R, r_col, c.col_start_local);
+}
+
+Ctx* as_ctx(pmf_ctx* p) {
+    if (!p) invalid("context is null");
+    return reinterpret_cast<Ctx*>(p);
+}
+
+}  // namespace pmfgpu
+
+using namespace pmfgpu;
+
+extern "C" {
+
+const char* pmf_last_error(void) { return g_err.c_str(); }
+int32_t pmf_abi_version(void) { return PMF_ABI_VERSION; }
+int32_t pmf_device_count(void) {
+    int c = 0;
+    if (cudaGetDeviceCount(&c) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return c;
+}
+
+pmf_status pmf_ctx_create(const pmf_matrix_view* a, int32_t device, pmf_ctx** out) {
+    return guard([&] {
+        if (!out) invalid("out is null");
+        auto c = make_ctx(a, device, 0, 1, nullptr);
+        build_als(*c, a);
+        *out = reinterpret_cast<pmf_ctx*>(c.release());
+    });
+}
+
+pmf_status pmf_ctx_create_dist(const pmf_matrix_view* a, int32_t device, int32_t rank, int32_t world,
+                               const uint8_t* id, pmf_ctx** out) {
+    return guard([&] {
+        if (!out) invalid("out is null");
+        if (world < 1 || rank < 0 || rank >= world) invalid("invalid rank / world");
+        if (world > 1 && !id) invalid("nccl id is null");
+        auto c = make_ctx(a, device, rank, world, id);
+        build_als(*c, a);
+        *out = reinterpret_cast<pmf_ctx*>(c.release());
+    });
+}
+
+pmf_status pmf_nccl_unique_id(uint8_t* out128) {
+    return guard([&] {
+        if (!out128) invalid("out is null");
+        ncclUniqueId id;
+        NCCL_TRY(ncclGetUniqueId(&id));
+        std::memcpy(out128, &id, sizeof(id));
+    });
+}
+
+pmf_status pmf_ctx_destroy(pmf_ctx* ctx) {
+    return guard([&] { delete as_ctx(ctx); });
+}
+
+pmf_status pmf_ctx_ccdpp_begin(pmf_ctx* ctx, const pmf_ccd_config* cfg) {
+    return guard([&] { ccd_begin(*as_ctx(ctx), cfg); });
+}
+pmf_status pmf_ctx_ccdpp_iterate(pmf_ctx* ctx, int32_t n_outer, double* secs) {
+    return guard([&] { ccd_iterate(*as_ctx(ctx), n_outer, secs); });
+}
+pmf_status pmf_ctx_als_begin(pmf_ctx* ctx, const pmf_als_config* cfg) {
+    return guard([&] { als_begin(*as_ctx(ctx), cfg); });
+}
+pmf_status pmf_ctx_als_iterate(pmf_ctx* ctx, int32_t n_outer, double* secs) {
+    return guard([&] { als_iterate(*as_ctx(ctx), n_outer, secs); });
+}
+pmf_status pmf_ctx_set_probe(pmf_ctx* ctx, const pmf_triplet* probe, int64_t n) {
+    return guard([&] { set_probe(*as_ctx(ctx), probe, n); });
+}
+pmf_status pmf_ctx_metrics(pmf_ctx* ctx, double* objective, double* rmse, double* train_rmse) {
+    return guard([&] { metrics(*as_ctx(ctx), objective, rmse, train_rmse); });
+}
+pmf_status pmf_ctx_get_model(pmf_ctx* ctx, float* W, float* H) {
+    return guard([&] { get_model(*as_ctx(ctx), W, H); });
+}
+pmf_status pmf_ctx_set_model(pmf_ctx* ctx, const float* W, const float* H, int32_t k) {
+    return guard([&] { set_model(*as_ctx(ctx), W, H, k); });
+}
+pmf_status pmf_ctx_get_residual(pmf_ctx* ctx, float* r_row, float* r_col) {
+    return guard([&] { get_residual(*as_ctx(ctx), r_row, r_col); });
+}
+pmf_status pmf_ctx_set_profiling(pmf_ctx* ctx, int32_t on) {
+    return guard([&] {
+        Ctx& c = *as_ctx(ctx);
+        c.profiling = on != 0;
+        reset_graph(c);
+    });
+}
+pmf_status pmf_ctx_launch_count(pmf_ctx* ctx, int64_t* per_iteration) {
+    return guard([&] {
+        if (!per_iteration) invalid("out is null");
+        *per_iteration = as_ctx(ctx)->launches_per_iter;
+    });
+}
+pmf_status pmf_ctx_kernel_stats(pmf_ctx* ctx, double* u_ms, int64_t* u_n, double* v_ms, int64_t* v_n) {
+    return guard([&] {
+        Ctx& c = *as_ctx(ctx);
+        if (u_ms) *u_ms = c.stat_u_ms;
+        if (u_n) *u_n = c.stat_u_n;
+        if (v_ms) *v_ms = c.stat_v_ms;
+        if (v_n) *v_n = c.stat_v_n;
+    });
+}
+
+}  // extern "C"
+
+template <class Begin, class Iterate>
+static pmf_status train_common(const pmf_matrix_view* a, int outer, const pmf_triplet* probe, int64_t n_probe,
+                               float* W_out, float* H_out, pmf_iter_row* rows, pmf_train_totals* totals,
+                               Begin begin, Iterate iterate) {
+    return guard([&] {
+        const double t0 = now_s();
+        if (!rows) invalid("rows_out is null");
+        if (n_probe < 0 || (n_probe > 0 && !probe)) invalid("probe is null");
+        check_view(a);
+        for (int64_t x = 0; x < n_probe; ++x)
+            if (probe[x].user < 0 || probe[x].user >= a->m || probe[x].item < 0 || probe[x].item >= a->n)
+                invalid("probe index outside training dimensions");
+        auto c = make_ctx(a, -1, 0, 1, nullptr);
+        begin(*c);
+        set_probe(*c, probe, n_probe);
+        double train = 0;
+        for (int it = 1; it <= outer; ++it) {
+            double s = 0;
+            iterate(*c, &s);
+            pmf_iter_row& r = rows[it - 1];
+            r.iteration = it;
+            r.seconds = s;
+            metrics(*c, &r.objective, &r.rmse, &r.train_rmse);
+            train += s;
+        }
+        get_model(*c, W_out, H_out);
+        if (totals) {
+            totals->train_seconds = train;
+            totals->final_objective = rows[outer - 1].objective;
+            totals->final_rmse = rows[outer - 1].rmse;
+            totals->setup_seconds = c->setup_seconds;
+            totals->h2d_bytes = c->h2d;
+            totals->d2h_bytes = c->d2h;
+            totals->kernel_launches = c->launches_per_iter * outer;
+            totals->wall_seconds = now_s() - t0;
+        }
+    });
+}
+
+extern "C" {
+
+pmf_status pmf_ccdpp_train(const pmf_ccd_config* cfg, const pmf_matrix_view* a, const pmf_triplet* probe,
+                           int64_t n_probe, float* W_out, float* H_out, pmf_iter_row* rows,
+                           pmf_train_totals* totals) {
+    if (!cfg) {
+        g_err = "config is null";
+        return PMF_INVALID_ARGUMENT;
+    }
+    return train_common(
+        a, cfg->outer_iters, probe, n_probe, W_out, H_out, rows, totals, [&](Ctx& c) { ccd_begin(c, cfg); },
+        [&](Ctx& c, double* s) { ccd_iterate(c, 1, s); });
+}
+
+pmf_status pmf_als_train(const pmf_als_config* cfg, const pmf_matrix_view* a, const pmf_triplet* probe,
+                         int64_t n_probe, float* W_out, float* H_out, pmf_iter_row* rows, pmf_train_totals* totals) {
+    if (!cfg) {
+        g_err = "config is null";
+        return PMF_INVALID_ARGUMENT;
+    }
+    if (cfg->outer_iters < 1 || cfg->k < 1 || !(cfg->lambda > 0.f)) {
+        g_err = cfg->outer_iters < 1 ? "outer_iters must be >= 1" : cfg->k < 1 ? "k must be >= 1" : "als requires lambda > 0";
+        return PMF_INVALID_ARGUMENT;
+    }
+    return train_common(
+        a, cfg->outer_iters, probe, n_probe, W_out, H_out, rows, totals,
+        [&](Ctx& c) {
+            build_als(c, a);
+            als_begin(c, cfg);
+        },
+        [&](Ctx& c, double* s) { als_iterate(c, 1, s); });
+}
+
+pmf_status pmf_rmse(const float* W, const float* H, int32_t m, int32_t n, int32_t k, const pmf_triplet* probe,
+                    int64_t n_probe, double* out) {
+    return guard([&] {
+        if (!W || !H || !out) invalid("null buffers");
+        if (k < 1) invalid("rank must be >= 1");
+        if (n_probe <= 0) invalid("probe set is empty");  // model.hpp:158-159
+        for (int64_t x = 0; x < n_probe; ++x) {
+            if (probe[x].user < 0 || probe[x].user >= m) throw PmfError(PMF_OUT_OF_RANGE, "user index out of range");
+            if (probe[x].item < 0 || probe[x].item >= n) throw PmfError(PMF_OUT_OF_RANGE, "item index out of range");
+        }
+        ensure_device();
+        cudaStream_t s;
+        CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        DevMem mem;
+        float* dW = mem.alloc<float>(static_cast<size_t>(m) * k, false);
+        float* dH = mem.alloc<float>(static_cast<size_t>(n) * k, false);
+        auto* dp = mem.alloc<DevTriplet>(n_probe, false);
+        double* scratch = mem.alloc<double>(2048);
+        double* res = mem.alloc<double>(1);
+        CUDA_TRY(cudaMemcpyAsync(dW, W, sizeof(float) * m * k, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(dH, H, sizeof(float) * n * k, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaMemcpyAsync(dp, probe, sizeof(pmf_triplet) * n_probe, cudaMemcpyHostToDevice, s));
+        launch_probe_sse(dp, n_probe, FactorView{dW, k, 1}, FactorView{dH, k, 1}, k, scratch, res, s);
+        double sse = 0;
+        CUDA_TRY(cudaMemcpyAsync(&sse, res, sizeof(double), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        cudaStreamDestroy(s);
+        *out = std::sqrt(sse / static_cast<double>(n_probe));  // rmse_finish, model.hpp:149-151
+    });
+}
+
+pmf_status pmf_objective(const pmf_matrix_view* a, const float* W, const float* H, int32_t k, double lambda,
+                         double* out) {
+    return guard([&] {
+        if (!W || !H || !out) invalid("null buffers");
+        if (lambda < 0) invalid("lambda must be >= 0");  // model.hpp:122
+        if (k < 1) invalid("rank must be >= 1");
+        auto c = make_ctx(a, -1, 0, 1, nullptr);
+        alloc_ccd_model(*c, k);
+        c->mode = 1;
+        set_model(*c, W, H, k);
+        c->lambda = 0.f;
+        double obj = 0;
+        metrics(*c, &obj, nullptr, nullptr);
+        // recompute with the double lambda given by the caller: obj == loss when lambda == 0
+        double h[3];
+        CUDA_TRY(cudaMemcpy(h, c->red_out, sizeof(h), cudaMemcpyDeviceToHost));
+        *out = h[0] + lambda * (h[1] + h[2]);
+    });
+}
+
+// ---- stage-level entry points -------------------------------------------------------------------
+
+pmf_status pmf_ccdpp_update_u(const pmf_matrix_view* a, const float* rhat_row, float* u, const float* v,
+                              float lambda) {
+    return guard([&] {
+        if (!rhat_row && a && a->nnz) invalid("null buffers");
+        if (!u || !v) invalid("null buffers");
+        auto c = make_ctx(a, -1, 0, 1, nullptr);
+        alloc_ccd_model(*c, 1);
+        put_values(*c, c->hcsr, c->csr.R, rhat_row, c->row_start_local);
+        CUDA_TRY(cudaMemcpy(c->vbuf, v, sizeof(float) * c->n, cudaMemcpyHostToDevice));
+        SweepOperands op;
+        op.gn = c->vbuf;
+        op.out = c->ubuf;
+        op.lambda = lambda;
+        launch_sweep(c->csr, kPlain, true, op, c->stream);
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        CUDA_TRY(cudaMemcpy(u, c->ubuf, sizeof(float) * c->m, cudaMemcpyDeviceToHost));
+    });
+}
+
+pmf_status pmf_ccdpp_update_v(const pmf_matrix_view* a, const float* rhat_col, const float* u, float* v,
+                              float lambda) {
+    return guard([&] {
+        if (!rhat_col && a && a->nnz) invalid("null buffers");
+        if (!u || !v) invalid("null buffers");
+        auto c = make_ctx(a, -1, 0, 1, nullptr);
+        alloc_ccd_model(*c, 1);
+        put_values(*c, c->hcsc, c->csc.R, rhat_col, c->col_start_local);
+        CUDA_TRY(cudaMemcpy(c->ubuf, u, sizeof(float) * c->m, cudaMemcpyHostToDevice));
+        SweepOperands op;
+        op.gn = c->ubuf;
+        op.out = c->vbuf;
+        op.lambda = lambda;
+        launch_sweep(c->csc, kPlain, false, op, c->stream);
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        CUDA_TRY(cudaMemcpy(v, c->vbuf, sizeof(float) * c->n, cudaMemcpyDeviceToHost));
+    });
+}
+
+// shared body of build_rhat / writeback: runs the fused promote (build) or demote (writeback)
+static void residual_stage(const pmf_matrix_view* a, float* r_row, float* r_col, const float* u, const float* v,
+                           bool build) {
+    if ((!r_row || !r_col) && a && a->nnz) invalid("null buffers");
+    if (!u || !v) invalid("null buffers");
+    auto c = make_ctx(a, -1, 0, 1, nullptr);
+    alloc_ccd_model(*c, 2);  // column 0: (u', v') = 0, column 1: (w, h) = (u, v)
+    put_values(*c, c->hcsr, c->csr.R, r_row, c->row_start_local);
+    put_values(*c, c->hcsc, c->csc.R, r_col, c->col_start_local);
+    float* W0 = c->W;
+    float* W1 = c->W + c->ldm;
+    float* H0 = c->H;
+    float* H1 = c->H + c->ldn;
+    CUDA_TRY(cudaMemcpy(build ? W1 : W0, u, sizeof(float) * c->m, cudaMemcpyHostToDevice));
+    CUDA_TRY(cudaMemcpy(build ? H1 : H0, v, sizeof(float) * c->n, cudaMemcpyHostToDevice));
+    SweepOperands o1, o2;
+    o1.oa = W0; o1.ga = H0; o1.ob = W1; o1.gb = H1; o1.gn = H1; o1.out = c->ubuf;
+    o2.oa = H0; o2.ga = W0; o2.ob = H1; o2.gb = W1; o2.gn = c->ubuf; o2.out = c->vbuf;
+    launch_sweep(c->csr, build ? kPromote : kDemote, true, o1, c->stream);
+    launch_sweep(c->csc, build ? kPromote : kDemote, false, o2, c->stream);
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    get_values(*c, c->hcsr, c->csr.R, r_row, c->row_start_local);
+    get_values(*c, c->hcsc, c->csc.R, r_col, c->col_start_local);
+}
+
+pmf_status pmf_ccdpp_build_rhat(const pmf_matrix_view* a, float* r_row, float* r_col, const float* u,
+                                const float* v) {
+    return guard([&] { residual_stage(a, r_row, r_col, u, v, true); });
+}
+
+pmf_status pmf_ccdpp_writeback(const pmf_matrix_view* a, float* r_row, float* r_col, const float* u,
+                               const float* v) {
+    return guard([&] { residual_stage(a, r_row, r_col, u, v, false); });
+}
+
+pmf_status pmf_als_solve_rows(const pmf_matrix_view* a, int32_t side, const float* opposing, int32_t k, float lambda,
+                              float* out) {
+    return guard([&] {
+        if (side != 0 && side != 1) invalid("side must be 0 (users) or 1 (items)");
+        if (!opposing || !out) invalid("null buffers");
+        if (k < 1) invalid("k must be >= 1");
+        if (k > 64) invalid("the B200 ALS kernels support k <= 64");
+        if (lambda < 0.f) invalid("lambda must be >= 0");
+        auto c = make_ctx(a, -1, 0, 1, nullptr);
+        build_als(*c, a);
+        c->k = k;
+        float* opp = c->model_mem.alloc<float>(static_cast<size_t>((side == 0 ? c->n : c->m) + 1) * k, false);
+        float* dst = c->model_mem.alloc<float>(static_cast<size_t>((side == 0 ? c->m : c->n) + 1) * k);
+        als_alloc_partials(*c, k);
+        CUDA_TRY(cudaMemcpy(opp, opposing, sizeof(float) * (side == 0 ? c->n : c->m) * k, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemset(c->d_status, 0, sizeof(int)));
+        launch_als_half(side == 0 ? c->als_csr : c->als_csc, opp, dst, 0, k, lambda, false, c->d_counter, c->d_status,
+                        c->sm_count, c->stream);
+        CUDA_TRY(cudaStreamSynchronize(c->stream));
+        int st = 0;
+        CUDA_TRY(cudaMemcpy(&st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+        if (st == 4) throw PmfError(PMF_NOT_POSITIVE_DEFINITE, "non-positive pivot in an ALS row solve");
+        CUDA_TRY(cudaMemcpy(out, dst, sizeof(float) * (side == 0 ? c->m : c->n) * k, cudaMemcpyDeviceToHost));
+    });
+}
+
+pmf_status pmf_cholesky_solve_batched(int32_t batch, int32_t k, float* a, float* x) {
+    return guard([&] {
+        if (batch < 0 || k < 1) invalid("invalid batch / order");
+        if (k > 64) invalid("the B200 batched Cholesky supports k <= 64");
+        if (batch == 0) return;
+        if (!a || !x) invalid("null buffers");
+        ensure_device();
+        static bool attrs = false;
+        if (!attrs) {
+            als_set_attributes();
+            attrs = true;
+        }
+        DevMem mem;
+        float* da = mem.alloc<float>(static_cast<size_t>(batch) * k * k, false);
+        float* dx = mem.alloc<float>(static_cast<size_t>(batch) * k, false);
+        int* st = mem.alloc<int>(1);
+        CUDA_TRY(cudaMemcpy(da, a, sizeof(float) * batch * k * k, cudaMemcpyHostToDevice));
+        CUDA_TRY(cudaMemcpy(dx, x, sizeof(float) * batch * k, cudaMemcpyHostToDevice));
+        launch_cholesky_batched(da, dx, batch, k, st, 0);
+        CUDA_TRY(cudaDeviceSynchronize());
+        int h = 0;
+        CUDA_TRY(cudaMemcpy(&h, st, sizeof(int), cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(a, da, sizeof(float) * batch * k * k, cudaMemcpyDeviceToHost));
+        CUDA_TRY(cudaMemcpy(x, dx, sizeof(float) * batch * k, cudaMemcpyDeviceToHost));
+        if (h == 4) throw PmfError(PMF_NOT_POSITIVE_DEFINITE, "non-positive pivot");
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,136 @@
+"""GPU parity tests for the ALS path (als.hpp:47-233, dense.hpp:35-124) through the C-ABI."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import frob_rel, rel
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "reference_trajectories.json")))
+
+
+def test_solve_rows_known_answers(pmf):
+    # als_test.cpp:14-20: empty row -> zero vector
+    A = pmf.RatingsMatrix.from_triplets([(1, 0, 4.0)], 3, 2)
+    w = pmf.solve_user_rows(A, np.full((2, 2), 0.5, np.float32), 2, 0.1)
+    assert np.all(w[0] == 0.0) and np.all(w[2] == 0.0)
+    # als_test.cpp:22-29: k=1, A=4, h=2 -> w = 8/(4+lambda)
+    A1 = pmf.RatingsMatrix.from_triplets([(0, 0, 4.0)], 1, 1)
+    w = pmf.solve_user_rows(A1, np.array([[2.0]], np.float32), 1, 1e-6)
+    assert abs(w[0, 0] - 8.0 / (4.0 + 1e-6)) < 1e-6
+    h = pmf.solve_item_rows(A1, np.array([[2.0]], np.float32), 1, 1e-6)   # als_test.cpp:55-60
+    assert abs(h[0, 0] - 2.0) < 1e-5
+
+
+def test_solve_rows_normal_equations(pmf, oracle):
+    """als_test.cpp:87-117: residual of (H^T H + lambda I) w = H^T a_i, against an independent solve."""
+    rng = np.random.default_rng(21)
+    for rep in range(5):
+        t = oracle.random_triplets(12, 9, 40, 100 + rep)
+        A = pmf.RatingsMatrix.from_triplets(t, 12, 9)
+        for k in (2, 3, 10):
+            h = rng.uniform(-1, 1, (9, k)).astype(np.float32)
+            w = pmf.solve_user_rows(A, h, k, 0.15)
+            for i in range(12):
+                js = A.col_of[A.row_start[i]:A.row_start[i + 1]]
+                a = A.val_row[A.row_start[i]:A.row_start[i + 1]].astype(np.float64)
+                Hs = h[js].astype(np.float64)
+                G = Hs.T @ Hs + 0.15 * np.eye(k)
+                r = G @ w[i].astype(np.float64) - Hs.T @ a
+                assert np.max(np.abs(r)) < 2e-4 * max(1.0, np.max(np.abs(Hs.T @ a)))
+
+
+@pytest.mark.parametrize("k", [1, 3, 8, 10, 16, 20, 32, 40, 50, 64])
+def test_solve_rows_vs_oracle(pmf, oracle, k):
+    t = oracle.synth_ratings(200, 120, 3, 6000, 7)
+    A = pmf.RatingsMatrix.from_triplets(t, 200, 120)
+    O = oracle.from_triplets(t, 200, 120)
+    rng = np.random.default_rng(k)
+    h = (rng.uniform(0, 1, (120, k)) / math.sqrt(k)).astype(np.float32)
+    w_gpu = pmf.solve_user_rows(A, h, k, 0.05)
+    w_ref = oracle.als_half(O, 0, h, 0.05)
+    assert frob_rel(w_gpu, w_ref) < 2e-3
+    hh = pmf.solve_item_rows(A, w_ref, k, 0.05)
+    h_ref = oracle.als_half(O, 1, w_ref, 0.05)
+    assert frob_rel(hh, h_ref) < 2e-3
+
+
+def test_long_columns_use_chunked_partials(pmf, oracle):
+    """Columns longer than the 4096-entry chunk go through the fixed-order partial reduction."""
+    m, n = 20000, 40
+    t = oracle.synth_ratings(m, n, 3, 200000, 5)
+    A = pmf.RatingsMatrix.from_triplets(t, m, n)
+    O = oracle.from_triplets(t, m, n)
+    assert np.diff(A.col_start).max() > 4096
+    rng = np.random.default_rng(0)
+    w = (rng.uniform(0, 1, (m, 10)) / math.sqrt(10)).astype(np.float32)
+    h_gpu = pmf.solve_item_rows(A, w, 10, 0.05)
+    h_ref = oracle.als_half(O, 1, w, 0.05)
+    assert frob_rel(h_gpu, h_ref) < 1e-3
+
+
+def test_als_ml100k_trajectory(pmf, oracle, ml100k):
+    train, probe = ml100k
+    A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
+    model, rep = pmf.als_train(pmf.AlsConfig(k=10, lam=0.05, outer_iters=5, seed=1), A, probe)
+    for r, g, gd in zip(rep.rows, GOLD["als_ml100k_k10_f32"]["rows"], GOLD["als_ml100k_k10_f64"]["rows"]):
+        for f in ("objective", "rmse", "train_rmse"):
+            assert rel(getattr(r, f), g[f]) < 1e-4, (f, r, g)
+            assert rel(getattr(r, f), gd[f]) < 1e-4, (f, r, gd)
+    O = oracle.from_triplets(train, 943, 1682)
+    W, H, _ = oracle.als_train(O, 10, 0.05, 5, 1, probe)
+    assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+
+
+def test_als_one_by_one_scalar_formulas(pmf):
+    """als_test.cpp:119-135: two half steps of the 1x1 problem."""
+    A = pmf.RatingsMatrix.from_triplets([(0, 0, 3.0)], 1, 1)
+    model, _ = pmf.als_train(pmf.AlsConfig(k=1, lam=0.5, outer_iters=1, seed=7), A)
+    h0 = float(pmf.init_random_items(1, 1, 7)[0, 0])
+    w1 = 3.0 * h0 / (h0 * h0 + 0.5)
+    h1 = 3.0 * w1 / (w1 * w1 + 0.5)
+    assert abs(model.w[0, 0] - w1) < 1e-5 and abs(model.h[0, 0] - h1) < 1e-5
+
+
+def test_als_planted_and_monotone(pmf, oracle):
+    t = oracle.planted_full(20, 15, 2, 0.01, 42)
+    A = pmf.RatingsMatrix.from_triplets(t, 20, 15)
+    _, rep = pmf.als_train(pmf.AlsConfig(k=2, lam=1e-6, outer_iters=15, seed=3), A)
+    assert rep.final_objective <= 1e-6
+    t = oracle.random_triplets(30, 20, 200, 77)
+    A = pmf.RatingsMatrix.from_triplets(t, 30, 20)
+    _, rep = pmf.als_train(pmf.AlsConfig(k=3, lam=0.1, outer_iters=15, seed=11), A)
+    objs = [r.objective for r in rep.rows]
+    assert all(b <= a * (1 + 1e-5) for a, b in zip(objs, objs[1:]))
+
+
+def test_als_validation(pmf, oracle):
+    t = oracle.random_triplets(5, 5, 10, 1)
+    A = pmf.RatingsMatrix.from_triplets(t, 5, 5)
+    with pytest.raises(ValueError):
+        pmf.als_train(pmf.AlsConfig(lam=0.0), A)           # als.hpp:36
+    with pytest.raises(ValueError):
+        pmf.als_train(pmf.AlsConfig(outer_iters=0), A)
+    with pytest.raises(ValueError):
+        pmf.als_train(pmf.AlsConfig(), A, [(9, 0, 1.0)])
+
+
+def test_cholesky_batched_known_answers(pmf, oracle):
+    L, x = pmf.cholesky_solve_batched(np.array([[4.0, 2.0], [2.0, 3.0]]), np.array([4.0, 5.0]))
+    np.testing.assert_allclose(L[0], [[2.0, 0.0], [1.0, math.sqrt(2.0)]], rtol=1e-6)   # dense_test.cpp:83-100
+    np.testing.assert_allclose(x[0], [0.25, 1.5], rtol=1e-6)                          # dense_test.cpp:158-170
+    with pytest.raises(ArithmeticError):
+        pmf.cholesky_solve_batched(np.array([[1.0, 2.0], [2.0, 1.0]]), np.array([1.0, 1.0]))
+    rng = np.random.default_rng(606)   # acceptance C10 in FP32: reconstruction and solve residual
+    for k in (1, 2, 5, 10, 40):
+        b = rng.uniform(-1, 1, (16, k, k))
+        spd = b @ np.transpose(b, (0, 2, 1)) + 0.1 * np.eye(k)
+        rhs = rng.uniform(-5, 5, (16, k))
+        L, x = pmf.cholesky_solve_batched(spd, rhs)
+        recon = L.astype(np.float64) @ np.transpose(L.astype(np.float64), (0, 2, 1))
+        assert np.max(np.abs(recon - spd)) < 1e-4 * max(1.0, np.max(np.abs(spd)))
+        res = np.einsum("bij,bj->bi", spd, x.astype(np.float64)) - rhs
+        assert np.max(np.abs(res)) < 5e-3 * np.max(np.abs(rhs)) * k
