@@ -1,20 +1,23 @@
 // ccd_kernels.cu -- CCD++ rank-one sweeps for sm_100a.
 //
 // One persistent CTA per SM walks its pieces (contiguous unit runs inside one gather panel,
-// layout.cpp).  Per piece it stages the panel's slice of the gather vectors (v, or u, plus the
-// promote/demote factors) into shared memory, then its warps pull work units from a shared
-// counter.  A warp streams its unit with 128-bit loads (4 residual values + 4 panel-local indices
-// per lane per step), gathers the factor values from shared memory and accumulates
-// num = sum R*g and den = sum g*g (ccd.hpp:165-171 / :188-194) in FP32, then reduces with a
-// fixed xor-shuffle tree.  On the first inner sweep of a rank-one step (kPromote) the residual is
-// rewritten in the same pass:  R <- (R - u'_i v'_j) [deferred writeback of the previous step,
-// ccd.hpp:213-214] then, if w_i != 0, R <- R + w_i h_j [build-rhat, ccd.hpp:142-147], each product
-// rounded before the add exactly like the reference (no FMA contraction), so the CSR and CSC
-// copies stay bitwise equal without the reference's cross-link mirror (sparse.hpp:241-250).
+// layout.cpp).  Per piece, one thread stages the panel's slice of the gather vectors (v, or u, plus
+// the promote/demote factors) into shared memory with TMA bulk copies (cp.async.bulk completing on
+// an mbarrier).  Warps then pull batches of 32/G work units from a shared counter; each group of G
+// lanes owns one unit, so a warp works on 32/G units at once, converged.  Every lane keeps U
+// independent 128-bit loads in flight (4 residual values + 4 panel-local indices each), gathers the
+// factor values from shared memory and accumulates num = sum R*g and den = sum g*g
+// (ccd.hpp:165-171 / :188-194) in FP32, then the group reduces with a fixed xor-shuffle tree.  The
+// next batch's descriptors are fetched before the current batch is processed.
+//
+// On the first inner sweep of a rank-one step (kPromote) the residual is rewritten in the same pass:
+// R <- (R - u'_i v'_j) [deferred writeback of the previous step, ccd.hpp:213-214] then, if w_i != 0,
+// R <- R + w_i h_j [build-rhat, ccd.hpp:142-147]; each product is rounded before the add exactly like
+// the reference (no FMA contraction), so the CSR and CSC copies stay bitwise equal without the
+// reference's cross-link mirror (sparse.hpp:241-250).
 #include <cuda_runtime.h>
 
 #include <algorithm>
-
 #include <cstdint>
 
 #include "device.hpp"
@@ -23,37 +26,174 @@ namespace pmfgpu {
 
 namespace {
 
-constexpr int kThreads = 1024;
-constexpr int kWarps = kThreads / 32;
+constexpr int kThreads = 512;
+constexpr int kUnroll = 4;
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_addr(bar)),
+        "r"(phase)
+        : "memory");
+}
+
+// TMA bulk copy global -> shared, completion counted on `bar` (bytes multiple of 16, 16B aligned)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_addr(dst)),
+        "l"(src), "r"(bytes), "r"(smem_addr(bar))
+        : "memory");
+}
 
 template <bool IDX16>
 struct IdxVec;
 template <>
 struct IdxVec<true> {
-    __device__ __forceinline__ static void load(const void* base, int64_t e, int (&g)[4]) {
-        const uint2 raw = __ldcs(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(base) + e));
-        g[0] = raw.x & 0xffffu;
-        g[1] = raw.x >> 16;
-        g[2] = raw.y & 0xffffu;
-        g[3] = raw.y >> 16;
+    using raw_t = uint2;
+    __device__ __forceinline__ static raw_t load(const void* base, int64_t e) {
+        return __ldcs(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(base) + e));
+    }
+    __device__ __forceinline__ static int get(const raw_t& r, int q) {
+        const uint32_t w = q < 2 ? r.x : r.y;
+        return (q & 1) ? static_cast<int>(w >> 16) : static_cast<int>(w & 0xffffu);
     }
 };
 template <>
 struct IdxVec<false> {
-    __device__ __forceinline__ static void load(const void* base, int64_t e, int (&g)[4]) {
-        const int4 raw = __ldcs(reinterpret_cast<const int4*>(static_cast<const int32_t*>(base) + e));
-        g[0] = raw.x;
-        g[1] = raw.y;
-        g[2] = raw.z;
-        g[3] = raw.w;
+    using raw_t = int4;
+    __device__ __forceinline__ static raw_t load(const void* base, int64_t e) {
+        return __ldcs(reinterpret_cast<const int4*>(static_cast<const int32_t*>(base) + e));
+    }
+    __device__ __forceinline__ static int get(const raw_t& r, int q) {
+        return q == 0 ? r.x : q == 1 ? r.y : q == 2 ? r.z : r.w;
     }
 };
 
-template <int MODE, bool CSR, bool SMEM>
-struct Gather {
-    // number of staged arrays
-    static constexpr int kArrays = MODE == kPlain ? 1 : MODE == kDemote ? 1 : (CSR ? 2 : 3);
+template <int MODE, bool CSR>
+struct Roles {
+    // staged arrays: plain: s0 = gn;  promote CSR: s0 = ga, s1 = gb (gn == gb);
+    // promote CSC: s0 = ga, s1 = gb, s2 = gn;  demote: s0 = ga.
+    static constexpr int kArrays = MODE == kPromote ? (CSR ? 2 : 3) : 1;
 };
+
+__host__ __device__ __forceinline__ int stage_stride(int panel_size) { return ((panel_size + 1) + 3) & ~3; }
+
+// Processes units [ub, ue) of the current piece in warp batches of 32/G units, one unit per group
+// of G lanes.  `counter` is the piece's shared counter for this length class.
+template <int MODE, bool CSR, bool IDX16, int G>
+__device__ __forceinline__ void run_class(int* counter, int32_t ub, int32_t ue, const Unit* __restrict__ units,
+                                          const void* __restrict__ idx, float* __restrict__ R,
+                                          float2* __restrict__ partial, const SweepOperands& op,
+                                          const float* g0, const float* g1, const float* g2) {
+    using IV = IdxVec<IDX16>;
+    constexpr int B = 32 / G;  // units per warp batch
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G;   // group within the warp
+    const int gl = lane % G;  // lane within the group
+    if (ub >= ue) return;
+    int nb = 0;
+    if (lane == 0) nb = atomicAdd(counter, B);
+    nb = __shfl_sync(0xffffffffu, nb, 0);
+    Unit Un = (nb + g < ue) ? units[nb + g] : Unit{0u, 0, 0, -2};
+    while (nb < ue) {
+        const Unit U = Un;
+        // prefetch the next batch's descriptors while this one streams
+        if (lane == 0) nb = atomicAdd(counter, B);
+        nb = __shfl_sync(0xffffffffu, nb, 0);
+        Un = (nb + g < ue) ? units[nb + g] : Unit{0u, 0, 0, -2};
+
+        const int32_t oidx = op.out_off + U.o;
+        float oa = 0.f, ob = 0.f;
+        if (MODE != kPlain && U.len > 0) oa = __ldg(op.oa + oidx);
+        if (MODE == kPromote && U.len > 0) ob = __ldg(op.ob + oidx);
+        const int64_t end = static_cast<int64_t>(U.e0) + U.len;
+        const int my_steps = (U.len + 4 * G * kUnroll - 1) / (4 * G * kUnroll);
+        const int steps = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_steps)));
+        float num = 0.f, den = 0.f;
+        for (int s = 0; s < steps; ++s) {
+            float4 r4[kUnroll];
+            typename IV::raw_t ix[kUnroll];
+            const int64_t base = static_cast<int64_t>(U.e0) + 4 * (gl + G * kUnroll * s);
+            // one base pointer per stream + immediate offsets; predicate on the remaining length
+            const int rem = static_cast<int>(end - base);
+            float4* rp = reinterpret_cast<float4*>(R + base);
+            const typename IV::raw_t* ip = reinterpret_cast<const typename IV::raw_t*>(
+                static_cast<const char*>(idx) + base * (IDX16 ? 2 : 4));
+#pragma unroll
+            for (int q = 0; q < kUnroll; ++q) {
+                if (4 * G * q < rem) {
+                    r4[q] = __ldcs(rp + G * q);
+                    ix[q] = __ldcs(ip + G * q);
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < kUnroll; ++q) {
+                if (4 * G * q < rem) {
+                    float rv[4] = {r4[q].x, r4[q].y, r4[q].z, r4[q].w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int gi = IV::get(ix[q], c);
+                        float r = rv[c];
+                        if (MODE == kPlain) {
+                            const float gv = g0[gi];
+                            num = fmaf(r, gv, num);
+                            den = fmaf(gv, gv, den);
+                        } else if (MODE == kDemote) {
+                            r = __fsub_rn(r, __fmul_rn(oa, g0[gi]));
+                        } else {
+                            const float a = g0[gi];
+                            const float b = g1[gi];
+                            // deferred writeback of the previous step: R - u'_i v'_j
+                            r = __fsub_rn(r, __fmul_rn(oa, a));
+                            // build-rhat, skipped when w_i == 0 (ccd.hpp:142)
+                            const float w = CSR ? ob : b;
+                            const float h = CSR ? b : ob;
+                            if (w != 0.f) r = __fadd_rn(r, __fmul_rn(w, h));
+                            const float gv = CSR ? b : g2[gi];
+                            num = fmaf(r, gv, num);
+                            den = fmaf(gv, gv, den);
+                        }
+                        rv[c] = r;
+                    }
+                    if (MODE != kPlain) __stcs(rp + G * q, make_float4(rv[0], rv[1], rv[2], rv[3]));
+                }
+            }
+        }
+        if (MODE == kDemote) continue;
+#pragma unroll
+        for (int off = G / 2; off > 0; off >>= 1) {
+            num += __shfl_xor_sync(0xffffffffu, num, off);
+            den += __shfl_xor_sync(0xffffffffu, den, off);
+        }
+        if (gl == 0 && U.len > 0) {
+            if (U.slot < 0) {
+                const float dt = __fadd_rn(op.lambda, den);
+                op.out[oidx] = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+            } else {
+                partial[U.slot] = make_float2(num, den);
+            }
+        }
+    }
+}
 
 template <int MODE, bool CSR, bool IDX16, bool SMEM>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -61,117 +201,53 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
              const int32_t* __restrict__ piece_start, const int32_t* __restrict__ panel_base,
              const void* __restrict__ idx, float* __restrict__ R, float2* __restrict__ partial,
              SweepOperands op, int32_t panel_size) {
-    extern __shared__ float smem[];
-    __shared__ int s_next;
-    constexpr int A = Gather<MODE, CSR, SMEM>::kArrays;
-    const int stride = panel_size + 1;
-    // staged array roles: plain: s0 = gn;  promote CSR: s0 = ga, s1 = gb (gn == gb);
-    // promote CSC: s0 = ga, s1 = gb, s2 = gn;  demote: s0 = ga.
+    extern __shared__ __align__(16) float smem[];
+    __shared__ int s_next[3];
+    __shared__ __align__(8) uint64_t s_bar;
+    constexpr int A = Roles<MODE, CSR>::kArrays;
+    const int stride = stage_stride(panel_size);
     float* s0 = smem;
     float* s1 = smem + stride;
     float* s2 = smem + 2 * stride;
-    const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+
+    if (SMEM && threadIdx.x == 0) mbar_init(&s_bar, 1);
+    uint32_t phase = 0;
 
     const int pb = piece_start[blockIdx.x], pe = piece_start[blockIdx.x + 1];
     for (int pc = pb; pc < pe; ++pc) {
         const Piece pz = pieces[pc];
-        int32_t gbase = 0;
-        __syncthreads();
-        if (SMEM) {
-            gbase = panel_base[pz.panel];
-            const int len = panel_base[pz.panel + 1] - gbase;
-            const float* src0 = MODE == kPlain ? op.gn : op.ga;
-            for (int x = threadIdx.x; x < len; x += kThreads) {
-                s0[x] = __ldg(src0 + gbase + x);
-                if (A >= 2) s1[x] = __ldg(op.gb + gbase + x);
-                if (A >= 3) s2[x] = __ldg(op.gn + gbase + x);
+        __syncthreads();  // previous piece fully consumed (and barrier initialised)
+        if (threadIdx.x == 0) {
+            s_next[0] = pz.ub;
+            s_next[1] = pz.um;
+            s_next[2] = pz.us;
+            if (SMEM) {
+                const int32_t gbase = panel_base[pz.panel];
+                const int len = panel_base[pz.panel + 1] - gbase;
+                const uint32_t bytes = static_cast<uint32_t>(((len + 3) & ~3) * sizeof(float));
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(&s_bar, bytes * A);
+                bulk_g2s(s0, (MODE == kPlain ? op.gn : op.ga) + gbase, bytes, &s_bar);
+                if (A >= 2) bulk_g2s(s1, op.gb + gbase, bytes, &s_bar);
+                if (A >= 3) bulk_g2s(s2, op.gn + gbase, bytes, &s_bar);
             }
+        }
+        if (SMEM) {
+            mbar_wait(&s_bar, phase);
+            phase ^= 1;
             if (threadIdx.x == 0) {
-                s0[panel_size] = 0.f;
+                s0[panel_size] = 0.f;  // sentinel slot of padding entries
                 if (A >= 2) s1[panel_size] = 0.f;
                 if (A >= 3) s2[panel_size] = 0.f;
             }
         }
-        if (threadIdx.x == 0) s_next = pz.ub;
         __syncthreads();
         const float* g0 = SMEM ? s0 : (MODE == kPlain ? op.gn : op.ga);
         const float* g1 = SMEM ? s1 : op.gb;
         const float* g2 = SMEM ? s2 : op.gn;
-        for (;;) {
-            int u = 0;
-            if (lane == 0) u = atomicAdd(&s_next, 1);
-            u = __shfl_sync(0xffffffffu, u, 0);
-            if (u >= pz.ue) break;
-            const Unit U = units[u];
-            const int32_t oidx = op.out_off + U.o;
-            float oa = 0.f, ob = 0.f;
-            if (MODE != kPlain) oa = __ldg(op.oa + oidx);
-            if (MODE == kPromote) ob = __ldg(op.ob + oidx);
-            float num = 0.f, den = 0.f;
-            const int64_t end = static_cast<int64_t>(U.e0) + U.len;
-            for (int64_t e = static_cast<int64_t>(U.e0) + 4 * lane; e < end; e += 256) {
-                const bool two = e + 128 < end;
-                float4 ra, rb;
-                int ia[4], ib[4];
-                ra = __ldcs(reinterpret_cast<const float4*>(R + e));
-                IdxVec<IDX16>::load(idx, e, ia);
-                if (two) {
-                    rb = __ldcs(reinterpret_cast<const float4*>(R + e + 128));
-                    IdxVec<IDX16>::load(idx, e + 128, ib);
-                }
-#pragma unroll
-                for (int half = 0; half < 2; ++half) {
-                    if (half == 1 && !two) break;
-                    float4& r4 = half == 0 ? ra : rb;
-                    const int(&gi)[4] = half == 0 ? ia : ib;
-                    float rv[4] = {r4.x, r4.y, r4.z, r4.w};
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int g = gi[q];
-                        float r = rv[q];
-                        if (MODE == kPlain) {
-                            const float gv = g0[g];
-                            num = fmaf(r, gv, num);
-                            den = fmaf(gv, gv, den);
-                        } else if (MODE == kDemote) {
-                            r = __fsub_rn(r, __fmul_rn(oa, g0[g]));
-                        } else {
-                            const float a = g0[g];
-                            const float b = g1[g];
-                            // deferred writeback of the previous step: R - u'_i v'_j
-                            r = __fsub_rn(r, __fmul_rn(oa, a));
-                            // build-rhat: skip when w_i == 0 (ccd.hpp:142)
-                            const float w = CSR ? ob : b;
-                            const float h = CSR ? b : ob;
-                            if (w != 0.f) r = __fadd_rn(r, __fmul_rn(w, h));
-                            const float gv = CSR ? b : g2[g];
-                            num = fmaf(r, gv, num);
-                            den = fmaf(gv, gv, den);
-                        }
-                        rv[q] = r;
-                    }
-                    if (MODE != kPlain) {
-                        float4 w4 = make_float4(rv[0], rv[1], rv[2], rv[3]);
-                        __stcs(reinterpret_cast<float4*>(R + e + 128 * half), w4);
-                    }
-                }
-            }
-            if (MODE == kDemote) continue;
-#pragma unroll
-            for (int off = 16; off > 0; off >>= 1) {
-                num += __shfl_xor_sync(0xffffffffu, num, off);
-                den += __shfl_xor_sync(0xffffffffu, den, off);
-            }
-            if (lane == 0) {
-                if (U.slot < 0) {
-                    const float dt = __fadd_rn(op.lambda, den);
-                    op.out[oidx] = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
-                } else {
-                    partial[U.slot] = make_float2(num, den);
-                }
-            }
-        }
+        run_class<MODE, CSR, IDX16, 8>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
+        run_class<MODE, CSR, IDX16, 4>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
+        run_class<MODE, CSR, IDX16, 2>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
     }
 }
 
@@ -221,8 +297,8 @@ void dispatch_idx(const DevSweep& L, const SweepOperands& op, size_t smem, cudaS
 
 template <int MODE, bool CSR, bool IDX16, bool SMEM>
 void set_attr(size_t max_smem) {
-    cudaFuncSetAttribute(sweep_kernel<MODE, CSR, IDX16, SMEM>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(max_smem));
+    cudaFuncSetAttribute(sweep_kernel<MODE, CSR, IDX16, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(max_smem));
 }
 
 template <int MODE, bool CSR>
@@ -238,7 +314,7 @@ void set_attr_all(size_t max_smem) {
 size_t sweep_smem_bytes(const DevSweep& L, SweepMode mode, bool csr_side) {
     if (!L.smem) return 0;
     const int arrays = mode == kPromote ? (csr_side ? 2 : 3) : 1;
-    return static_cast<size_t>(arrays) * (L.panel_size + 1) * sizeof(float);
+    return static_cast<size_t>(arrays) * stage_stride(L.panel_size) * sizeof(float);
 }
 
 void sweep_set_attributes(size_t max_smem) {

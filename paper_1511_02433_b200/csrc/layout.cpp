@@ -83,8 +83,9 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     auto gidx = [&](int64_t e) -> int32_t { return gmap ? gmap[idx[e]] : idx[e]; };
 
     // ---- 1. gather panels ------------------------------------------------------------------
-    int64_t pg_cap = smem_budget_bytes / (4 * stage_arrays) - 1;
-    if (allow_idx16) pg_cap = std::min<int64_t>(pg_cap, 65535);
+    // panel width: a multiple of 4 floats so every panel base is 16-byte aligned for the TMA copy
+    int64_t pg_cap = (smem_budget_bytes / (4 * stage_arrays) - 4) & ~int64_t(3);
+    if (allow_idx16) pg_cap = std::min<int64_t>(pg_cap, 65532);
     const int64_t nnz_side = start[out_end] - start[out_begin];
     L.n_real = nnz_side;
     if (gat_extent <= pg_cap) {
@@ -221,8 +222,26 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
         for (int64_t u = ub; u < ue;) {
             int64_t v = u;
             while (v < ue && L.unit_panel[v] == L.unit_panel[u]) ++v;
-            L.pieces.push_back(Piece{L.unit_panel[u], static_cast<int32_t>(u),
-                                     static_cast<int32_t>(v), 0});
+            // longest units first inside a piece: the 32/G units a warp takes together then have
+            // similar lengths (converged groups) and the long ones start early (LPT balance)
+            std::vector<int64_t> ord(v - u);
+            std::iota(ord.begin(), ord.end(), u);
+            std::stable_sort(ord.begin(), ord.end(),
+                             [&](int64_t a, int64_t b) { return L.units[a].len > L.units[b].len; });
+            std::vector<Unit> tu(v - u);
+            std::vector<int32_t> tr(v - u);
+            for (int64_t x = 0; x < v - u; ++x) {
+                tu[x] = L.units[ord[x]];
+                tr[x] = L.unit_real[ord[x]];
+            }
+            std::copy(tu.begin(), tu.end(), L.units.begin() + u);
+            std::copy(tr.begin(), tr.end(), L.unit_real.begin() + u);
+            int64_t um = u, us = u;
+            while (um < v && L.units[um].len > kMidLen) ++um;
+            us = um;
+            while (us < v && L.units[us].len > kShortLen) ++us;
+            L.pieces.push_back(Piece{L.unit_panel[u], static_cast<int32_t>(u), static_cast<int32_t>(um),
+                                     static_cast<int32_t>(us), static_cast<int32_t>(v), {0, 0, 0}});
             u = v;
         }
         L.piece_start[c + 1] = static_cast<int32_t>(L.pieces.size());
@@ -232,8 +251,15 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
 }
 
 void for_each_entry(const SweepLayout& L, const std::function<void(int32_t, int64_t, int64_t)>& fn) {
+    // an output's entries, in reference order, are its units sorted by entry offset (panels are
+    // laid out in ascending order, chunks of a segment are consecutive)
+    std::vector<int64_t> ord(L.units.size());
+    std::iota(ord.begin(), ord.end(), 0);
+    std::sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+        return L.units[a].o != L.units[b].o ? L.units[a].o < L.units[b].o : L.units[a].e0 < L.units[b].e0;
+    });
     std::vector<int64_t> run(L.n_out, 0);
-    for (size_t u = 0; u < L.units.size(); ++u) {
+    for (int64_t u : ord) {
         const Unit& U = L.units[u];
         for (int32_t x = 0; x < L.unit_real[u]; ++x)
             fn(U.o, run[U.o] + x, static_cast<int64_t>(U.e0) + x);

@@ -19,7 +19,7 @@
 namespace pmfgpu {
 
 constexpr int kUnitMax = 4096;      // entries per warp work unit (multiple of 128)
-constexpr int kUnitOverhead = 96;   // cost model: fixed per-unit overhead in "entries"
+constexpr int kUnitOverhead = 8;       // cost model: fixed per-unit overhead in "entries"
 
 // 16-byte work unit, read with one 128-bit load.
 struct Unit {
@@ -29,10 +29,16 @@ struct Unit {
     int32_t slot;  // -1: the only unit of its output (finalizes directly); else partial slot
 };
 
-struct Piece {   // a CTA's contiguous run of units inside one gather panel
+// A CTA's contiguous run of units inside one gather panel.  Units are sorted by length
+// (descending); [ub, um) are long units (> kMidLen entries, 8-lane groups), [um, us) medium
+// (4-lane groups), [us, ue) short (<= kShortLen, 2-lane groups), so short segments get more units
+// in flight per warp.
+constexpr int kMidLen = 128;
+constexpr int kShortLen = 64;
+struct Piece {
     int32_t panel;
-    int32_t ub, ue;
-    int32_t pad;
+    int32_t ub, um, us, ue;
+    int32_t pad[3];
 };
 
 struct SweepLayout {

@@ -259,8 +259,8 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     c->Bn = world == 1 ? a->n : bn;
     c->ext_m = world * c->Bm;
     c->ext_n = world * c->Bn;
-    c->ldm = ((c->ext_m + 1 + 31) / 32) * 32;
-    c->ldn = ((c->ext_n + 1 + 31) / 32) * 32;
+    c->ldm = ((c->ext_m + 4 + 31) / 32) * 32;  // slack: sentinel + TMA round-up
+    c->ldn = ((c->ext_n + 4 + 31) / 32) * 32;
     if (world > 1) {
         c->rmap.resize(a->m);
         c->cmap.resize(a->n);

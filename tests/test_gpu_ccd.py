@@ -58,7 +58,7 @@ def test_build_rhat_skip_and_oracle(pmf, oracle):
     rr, rc = pmf.ccdpp_build_rhat(A, r0, r0c, u, v)
     er, ec = oracle.build_rhat(O, r0, r0c, u, v)
     assert np.array_equal(rr, er) and np.array_equal(rc, ec)
-    assert np.array_equal(rr[O.xlink], rc)  # layouts bitwise equal through the cross-link
+    assert np.array_equal(rc[O.xlink], rr)  # layouts bitwise equal through the cross-link
     wr, wc = pmf.ccdpp_writeback(A, rr, rc, u, v)
     xr, xc, _, _ = oracle.writeback(O, er, ec, u, v)
     assert np.array_equal(wr, xr) and np.array_equal(wc, xc)
@@ -130,7 +130,7 @@ def test_small_exact_fixture_and_residual(pmf, oracle):
     assert frob_rel(model.w, np.array(g["W"]).reshape(40, 3)) < 1e-3
     assert frob_rel(model.h, np.array(g["H"]).reshape(30, 3)) < 1e-3
     rr, rc = ctx.residual()
-    assert np.array_equal(rr[O.xlink], rc)      # both layouts bitwise equal (testutil.hpp:266-272)
+    assert np.array_equal(rc[O.xlink], rr)      # both layouts bitwise equal (testutil.hpp:266-272)
     pred = np.einsum("ik,ik->i", model.w[np.repeat(np.arange(40), np.diff(O.row_start))].astype(np.float64),
                      model.h[O.col_of].astype(np.float64))
     assert np.max(np.abs(rr - (O.val_row - pred))) < 1e-4   # residual_max_error, FP32 band
