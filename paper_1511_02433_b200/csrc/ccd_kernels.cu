@@ -27,7 +27,6 @@ namespace pmfgpu {
 namespace {
 
 constexpr int kThreads = 512;
-constexpr int kUnroll = 4;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -99,8 +98,8 @@ __host__ __device__ __forceinline__ int stage_stride(int panel_size) { return ((
 
 // Processes units [ub, ue) of the current piece in warp batches of 32/G units, one unit per group
 // of G lanes.  `counter` is the piece's shared counter for this length class.
-template <int MODE, bool CSR, bool IDX16, int G>
-__device__ __forceinline__ void run_class(int* counter, int32_t ub, int32_t ue, const Unit* __restrict__ units,
+template <int MODE, bool CSR, bool IDX16, int G, int kUnroll>
+__device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, const Unit* __restrict__ units,
                                           const void* __restrict__ idx, float* __restrict__ R,
                                           float2* __restrict__ partial, const SweepOperands& op,
                                           const float* g0, const float* g1, const float* g2) {
@@ -245,9 +244,9 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
         const float* g0 = SMEM ? s0 : (MODE == kPlain ? op.gn : op.ga);
         const float* g1 = SMEM ? s1 : op.gb;
         const float* g2 = SMEM ? s2 : op.gn;
-        run_class<MODE, CSR, IDX16, 8>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
-        run_class<MODE, CSR, IDX16, 4>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
-        run_class<MODE, CSR, IDX16, 2>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
+        run_class<MODE, CSR, IDX16, 8, 8>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
+        run_class<MODE, CSR, IDX16, 4, 4>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
+        run_class<MODE, CSR, IDX16, 2, 4>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
     }
 }
 

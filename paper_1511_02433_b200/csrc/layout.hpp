@@ -18,7 +18,7 @@
 
 namespace pmfgpu {
 
-constexpr int kUnitMax = 4096;      // entries per warp work unit (multiple of 128)
+constexpr int kUnitMax = 1024;      // entries per warp work unit (multiple of 128)
 constexpr int kUnitOverhead = 8;       // cost model: fixed per-unit overhead in "entries"
 
 // 16-byte work unit, read with one 128-bit load.
