@@ -158,6 +158,11 @@ pmf_status pmf_ctx_kernel_stats(pmf_ctx* ctx, double* usweep_ms, int64_t* usweep
                                 double* vsweep_ms, int64_t* vsweep_launches);
 /* Kernels launched by one outer iteration of the active solver (CCD++ graph or ALS phases). */
 pmf_status pmf_ctx_launch_count(pmf_ctx* ctx, int64_t* per_iteration);
+/* Diagnostic: runs one sweep (side 0 = u over CSR, 1 = v over CSC; promote or plain) on a copy of the
+ * residual and returns per-CTA [start, end] globaltimer ns (2*ctas) and per-CTA layout stats
+ * (6*ctas: long/medium/short units, entries, pieces, last panel). */
+pmf_status pmf_ctx_debug_sweep_profile(pmf_ctx* ctx, int32_t side, int32_t promote, uint64_t* cta_ns,
+                                      int64_t* cta_stats, int32_t* n_ctas);
 /* Enables (1) / disables (0) per-sweep CUDA-event timing inside pmf_ctx_ccdpp_iterate. */
 pmf_status pmf_ctx_set_profiling(pmf_ctx* ctx, int32_t on);
 

@@ -113,6 +113,7 @@ _SIGS = {
     "pmf_ctx_kernel_stats": ([_P, _P, _P, _P, _P], C.c_int),
     "pmf_ctx_set_profiling": ([_P, C.c_int32], C.c_int),
     "pmf_ctx_launch_count": ([_P, _P], C.c_int),
+    "pmf_ctx_debug_sweep_profile": ([_P, C.c_int32, C.c_int32, _P, _P, _P], C.c_int),
     "pmf_ccdpp_build_rhat": ([_P, _P, _P, _P, _P], C.c_int),
     "pmf_ccdpp_update_u": ([_P, _P, _P, _P, C.c_float], C.c_int),
     "pmf_ccdpp_update_v": ([_P, _P, _P, _P, C.c_float], C.c_int),
@@ -661,6 +662,13 @@ class Context:
 
     def set_profiling(self, on: bool):
         _check(lib.pmf_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def debug_sweep_profile(self, side: int, promote: bool = False):
+        n = C.c_int32()
+        clk = np.zeros(2 * 1024, np.uint64); st = np.zeros(6 * 1024, np.int64)
+        _check(lib.pmf_ctx_debug_sweep_profile(self.h, side, 1 if promote else 0, _ptr(clk), _ptr(st), C.byref(n)))
+        c = n.value
+        return clk[:2 * c].reshape(c, 2), st[:6 * c].reshape(c, 6)
 
     def launch_count(self) -> int:
         n = C.c_int64()

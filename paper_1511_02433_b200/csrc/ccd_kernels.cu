@@ -209,6 +209,11 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
     float* s1 = smem + stride;
     float* s2 = smem + 2 * stride;
 
+    if (op.cta_clock && threadIdx.x == 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        op.cta_clock[2 * blockIdx.x] = t;
+    }
     if (SMEM && threadIdx.x == 0) mbar_init(&s_bar, 1);
     uint32_t phase = 0;
 
@@ -247,6 +252,14 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
         run_class<MODE, CSR, IDX16, 8, 8>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
         run_class<MODE, CSR, IDX16, 4, 4>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
         run_class<MODE, CSR, IDX16, 2, 4>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
+    }
+    if (op.cta_clock) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            op.cta_clock[2 * blockIdx.x + 1] = t;
+        }
     }
 }
 

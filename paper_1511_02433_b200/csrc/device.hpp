@@ -39,6 +39,7 @@ struct SweepOperands {
     const float* ob = nullptr;  // promote factor, per output(w  on CSR, h  on CSC)
     float* out = nullptr;       // result vector (u or v), written at out_off + o
     int32_t out_off = 0;
+    unsigned long long* cta_clock = nullptr;  // profiling: per-CTA [start, end] globaltimer (ns)
     float lambda = 0.f;
 };
 

@@ -827,6 +827,54 @@ pmf_status pmf_ctx_set_profiling(pmf_ctx* ctx, int32_t on) {
         reset_graph(c);
     });
 }
+pmf_status pmf_ctx_debug_sweep_profile(pmf_ctx* ctx, int32_t side, int32_t promote, uint64_t* cta_ns,
+                                      int64_t* cta_stats, int32_t* n_ctas) {
+    return guard([&] {
+        Ctx& c = *as_ctx(ctx);
+        if (c.mode != 1) invalid("ccdpp_begin has not been called");
+        const DevSweep& L = side == 0 ? c.csr : c.csc;
+        const SweepLayout& H = side == 0 ? c.hcsr : c.hcsc;
+        *n_ctas = L.ctas;
+        DevMem tmp;
+        auto* clk = tmp.alloc<unsigned long long>(2 * L.ctas);
+        SweepOperands op;
+        op.lambda = c.lambda;
+        op.cta_clock = clk;
+        const int t = 0, tp = c.k - 1;
+        if (side == 0) {
+            op.out = c.ubuf; op.out_off = c.rank * c.Bm;
+            op.gn = promote ? c.H : c.vbuf; op.ga = c.H + static_cast<int64_t>(tp) * c.ldn; op.gb = c.H;
+            op.oa = c.W + static_cast<int64_t>(tp) * c.ldm; op.ob = c.W;
+        } else {
+            op.out = c.vbuf; op.out_off = c.rank * c.Bn;
+            op.gn = c.ubuf; op.ga = c.W + static_cast<int64_t>(tp) * c.ldm; op.gb = c.W;
+            op.oa = c.H + static_cast<int64_t>(tp) * c.ldn; op.ob = c.H;
+        }
+        (void)t;
+        // work on a copy of R so the training state is untouched
+        DevSweep Lc = L;
+        Lc.R = tmp.alloc<float>(L.n_entries + 4, false);
+        CUDA_TRY(cudaMemcpyAsync(Lc.R, L.R, L.n_entries * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+        launch_sweep(Lc, promote ? kPromote : kPlain, side == 0, op, c.stream);
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        CUDA_TRY(cudaMemcpy(cta_ns, clk, sizeof(uint64_t) * 2 * L.ctas, cudaMemcpyDeviceToHost));
+        if (cta_stats) {
+            for (int x = 0; x < 6 * L.ctas; ++x) cta_stats[x] = 0;
+            for (int cc = 0; cc < L.ctas; ++cc)
+                for (int p = H.piece_start[cc]; p < H.piece_start[cc + 1]; ++p) {
+                    const Piece& pz = H.pieces[p];
+                    int64_t* st = cta_stats + 6 * cc;
+                    st[0] += pz.um - pz.ub;
+                    st[1] += pz.us - pz.um;
+                    st[2] += pz.ue - pz.us;
+                    for (int u = pz.ub; u < pz.ue; ++u) st[3] += H.units[u].len;
+                    st[4] += 1;
+                    st[5] = pz.panel;
+                }
+        }
+    });
+}
+
 pmf_status pmf_ctx_launch_count(pmf_ctx* ctx, int64_t* per_iteration) {
     return guard([&] {
         if (!per_iteration) invalid("out is null");

@@ -41,5 +41,31 @@ def main():
         print("als iter s:", list(ctx.als_iterate(a.als)), file=sys.stderr)
 
 
+
+
+def cta_profile():
+    """python scripts/profile_run.py --cta: per-CTA time spread of one plain u- and v-sweep."""
+    import numpy as np
+    train, probe, A = bench.make_data("netflix-ccdpp")
+    ctx = P.Context(A)
+    ctx.ccdpp_begin(P.CcdConfig(k=40, lam=0.05, outer_iters=1, inner_iters=15, seed=1))
+    ctx.ccdpp_iterate(1)
+    for side in (0, 1):
+        for promote in (False, True):
+            clk, st = ctx.debug_sweep_profile(side, promote)
+            t0 = clk[:, 0].min()
+            dur = (clk[:, 1] - clk[:, 0]) / 1e3
+            end = (clk[:, 1] - t0) / 1e3
+            print(f"side {side} promote {promote}: kernel {end.max():.1f} us; CTA dur min {dur.min():.1f} "
+                  f"avg {dur.mean():.1f} max {dur.max():.1f}; start spread {(clk[:, 0].max() - t0) / 1e3:.1f} us")
+            order = np.argsort(-dur)
+            for c in list(order[:6]) + list(order[-3:]):
+                print(f"   cta {c:3d} dur {dur[c]:7.1f} us  long {st[c, 0]:5d} mid {st[c, 1]:5d} short {st[c, 2]:5d} "
+                      f"entries {st[c, 3]:8d} pieces {st[c, 4]} panel {st[c, 5]}")
+
+
 if __name__ == "__main__":
-    main()
+    if "--cta" in sys.argv:
+        cta_profile()
+    else:
+        main()
