@@ -214,6 +214,13 @@ int32_t pmf_device_count(void);
 
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink / NVSwitch) -------------------------- */
 
+/* Host-only: the plan pmf_ctx_create_dist uses -- rank r owns CSR rows [row_bounds[r], row_bounds[r+1])
+ * and CSC columns [col_bounds[r], col_bounds[r+1]) (partition_balanced over 4|Omega|,
+ * runtime.hpp:73-136); replicated u/v/W/H live in a padded index space where block r occupies
+ * [r*B, (r+1)*B) with B = block_rows (users) or block_cols (items), so every NCCL all-gather uses
+ * equal counts.  row_bounds / col_bounds have world+1 entries. */
+pmf_status pmf_dist_plan(const pmf_matrix_view* a, int32_t world, int32_t* row_bounds, int32_t* col_bounds,
+                         int32_t* block_rows, int32_t* block_cols);
 /* 128-byte ncclUniqueId produced on rank 0 and broadcast by the caller (e.g. torch.distributed). */
 pmf_status pmf_nccl_unique_id(uint8_t* out128);
 /* Like pmf_ctx_create, but this rank owns the CSR row block and CSC column block chosen by

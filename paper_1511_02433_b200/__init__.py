@@ -43,7 +43,7 @@ __all__ = [
     "TrainReport", "ccdpp_train", "als_train", "Algorithm", "RunSpec", "run_training", "rmse", "objective",
     "predict", "init_random_items", "ccdpp_build_rhat", "ccdpp_update_u", "ccdpp_update_v", "ccdpp_writeback",
     "solve_user_rows", "solve_item_rows", "cholesky_solve_batched", "partition_balanced", "synth_ratings",
-    "Context", "DataError", "NotPositiveDefinite", "DomainError", "device_count", "nccl_unique_id",
+    "Context", "DataError", "NotPositiveDefinite", "DomainError", "device_count", "nccl_unique_id", "dist_plan",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -125,6 +125,7 @@ _SIGS = {
     "pmf_synth_ratings": ([C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_uint32, _P, _P, _P, _P],
                           C.c_int),
     "pmf_nccl_unique_id": ([_P], C.c_int),
+    "pmf_dist_plan": ([_P, C.c_int32, _P, _P, _P, _P], C.c_int),
 }
 
 
@@ -581,6 +582,14 @@ def synth_ratings(m, n, true_rank, n_train, n_probe, seed):
     return tr[:gt.value], pr[:gp.value]
 
 
+def dist_plan(a: RatingsMatrix, world: int):
+    """(row_bounds, col_bounds, block_rows, block_cols) used by multi-GPU contexts."""
+    rb = np.zeros(world + 1, np.int32); cb = np.zeros(world + 1, np.int32)
+    bm, bn = C.c_int32(), C.c_int32()
+    _check(lib.pmf_dist_plan(a.view(), world, _ptr(rb), _ptr(cb), C.byref(bm), C.byref(bn)))
+    return rb, cb, bm.value, bn.value
+
+
 def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(lib.pmf_nccl_unique_id(buf))
@@ -597,7 +606,7 @@ class Context:
     def __init__(self, a: RatingsMatrix, device: int = -1, rank: int = 0, world: int = 1, nccl_id: bytes = None):
         self.a = a
         self.h = C.c_void_p()
-        if world == 1:
+        if nccl_id is None:
             _check(lib.pmf_ctx_create(a.view(), device, C.byref(self.h)))
         else:
             idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)

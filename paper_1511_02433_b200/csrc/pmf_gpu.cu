@@ -217,6 +217,26 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     return D;
 }
 
+// Distribution plan shared by pmf_ctx_create_dist and pmf_dist_plan: rank r owns CSR rows
+// [row_bounds[r], row_bounds[r+1]) and CSC columns [col_bounds[r], col_bounds[r+1]); the replicated
+// vectors live in a padded space where block r occupies [r*B, (r+1)*B), B = largest block (so NCCL
+// all-gathers use equal counts).  world == 1 keeps the identity space.
+void dist_plan(const int64_t* row_start, int32_t m, const int64_t* col_start, int32_t n, int world,
+               int32_t* row_bounds, int32_t* col_bounds, int32_t* Bm, int32_t* Bn) {
+    std::vector<int64_t> rc(m), cc(n);
+    for (int32_t i = 0; i < m; ++i) rc[i] = 4 * (row_start[i + 1] - row_start[i]);
+    for (int32_t j = 0; j < n; ++j) cc[j] = 4 * (col_start[j + 1] - col_start[j]);
+    partition_balanced(rc.data(), m, world, row_bounds);
+    partition_balanced(cc.data(), n, world, col_bounds);
+    int32_t bm = 0, bn = 0;
+    for (int r = 0; r < world; ++r) {
+        bm = std::max(bm, row_bounds[r + 1] - row_bounds[r]);
+        bn = std::max(bn, col_bounds[r + 1] - col_bounds[r]);
+    }
+    *Bm = world == 1 ? m : bm;
+    *Bn = world == 1 ? n : bn;
+}
+
 std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, int world, const uint8_t* id) {
     check_view(a);
     ensure_device();
@@ -232,31 +252,18 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     c->nnz = a->nnz;
     c->rank = rank;
     c->world = world;
-    if (world > 1) {
+    if (id) {  // distributed context (a 1-rank communicator is allowed and exercises the same path)
         ncclUniqueId uid;
         std::memcpy(&uid, id, sizeof(uid));
         NCCL_TRY(ncclCommInitRank(&c->comm, world, uid, rank));
     }
-    // row / column blocks (runtime.hpp:73-136, 4|Omega| costs)
+    // row / column blocks (runtime.hpp:73-136, 4|Omega| costs) and the padded index space
     std::vector<int32_t> rb(world + 1), cbd(world + 1);
-    {
-        std::vector<int64_t> rc(a->m), cc(a->n);
-        for (int32_t i = 0; i < a->m; ++i) rc[i] = 4 * (a->row_start[i + 1] - a->row_start[i]);
-        for (int32_t j = 0; j < a->n; ++j) cc[j] = 4 * (a->col_start[j + 1] - a->col_start[j]);
-        partition_balanced(rc.data(), a->m, world, rb.data());
-        partition_balanced(cc.data(), a->n, world, cbd.data());
-    }
+    dist_plan(a->row_start, a->m, a->col_start, a->n, world, rb.data(), cbd.data(), &c->Bm, &c->Bn);
     c->row_begin = rb[rank];
     c->row_end = rb[rank + 1];
     c->col_begin = cbd[rank];
     c->col_end = cbd[rank + 1];
-    int32_t bm = 0, bn = 0;
-    for (int r = 0; r < world; ++r) {
-        bm = std::max(bm, rb[r + 1] - rb[r]);
-        bn = std::max(bn, cbd[r + 1] - cbd[r]);
-    }
-    c->Bm = world == 1 ? a->m : bm;
-    c->Bn = world == 1 ? a->n : bn;
     c->ext_m = world * c->Bm;
     c->ext_n = world * c->Bn;
     c->ldm = ((c->ext_m + 4 + 31) / 32) * 32;  // slack: sentinel + TMA round-up
@@ -352,7 +359,7 @@ void reset_residual(Ctx& c) {
 }
 
 void allgather(Ctx& c, float* buf, int64_t block) {
-    if (c.world > 1)
+    if (c.comm)
         NCCL_TRY(ncclAllGather(buf + static_cast<int64_t>(c.rank) * block, buf, block, ncclFloat, c.comm, c.stream));
 }
 
@@ -629,7 +636,7 @@ void metrics(Ctx& c, double* objective, double* rmse, double* train_rmse) {
     launch_sumsq(c.W, wn, c.red_scratch + 1024, c.red_out + 1, c.stream);
     launch_sumsq(c.H, hn, c.red_scratch + 2048, c.red_out + 2, c.stream);
     if (c.n_probe > 0) launch_probe_sse(c.probe, c.n_probe, W, H, c.k, c.red_scratch + 3072, c.red_out + 3, c.stream);
-    if (c.world > 1) NCCL_TRY(ncclAllReduce(c.red_out, c.red_out, 1, ncclDouble, ncclSum, c.comm, c.stream));
+    if (c.comm) NCCL_TRY(ncclAllReduce(c.red_out, c.red_out, 1, ncclDouble, ncclSum, c.comm, c.stream));
     double h[4] = {0, 0, 0, 0};
     CUDA_TRY(cudaMemcpyAsync(h, c.red_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
     CUDA_TRY(cudaStreamSynchronize(c.stream));
@@ -773,10 +780,20 @@ pmf_status pmf_ctx_create_dist(const pmf_matrix_view* a, int32_t device, int32_t
     return guard([&] {
         if (!out) invalid("out is null");
         if (world < 1 || rank < 0 || rank >= world) invalid("invalid rank / world");
-        if (world > 1 && !id) invalid("nccl id is null");
+        if (!id) invalid("nccl id is null");
         auto c = make_ctx(a, device, rank, world, id);
         build_als(*c, a);
         *out = reinterpret_cast<pmf_ctx*>(c.release());
+    });
+}
+
+pmf_status pmf_dist_plan(const pmf_matrix_view* a, int32_t world, int32_t* row_bounds, int32_t* col_bounds,
+                         int32_t* block_rows, int32_t* block_cols) {
+    return guard([&] {
+        check_view(a);
+        if (world < 1) invalid("world must be >= 1");
+        if (!row_bounds || !col_bounds || !block_rows || !block_cols) invalid("null buffers");
+        dist_plan(a->row_start, a->m, a->col_start, a->n, world, row_bounds, col_bounds, block_rows, block_cols);
     });
 }
 

@@ -192,3 +192,26 @@ def test_multi_panel_layout_vs_oracle(pmf, oracle):
     for r, g in zip(rep.rows, rows):
         assert rel(r.objective, g["objective"]) < 1e-4
     assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+
+
+def test_distributed_context_single_rank_nccl(pmf, ml100k):
+    """pmf_ctx_create_dist with a 1-rank NCCL communicator: the all-gathers run inside the captured
+    CUDA graph and the result equals the plain context bit-for-bit."""
+    train, probe = ml100k
+    A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
+    cfg = pmf.CcdConfig(k=5, lam=0.05, outer_iters=2, inner_iters=3, seed=2)
+    a = pmf.Context(A)
+    a.ccdpp_begin(cfg)
+    a.ccdpp_iterate(2)
+    b = pmf.Context(A, rank=0, world=1, nccl_id=pmf.nccl_unique_id())
+    b.ccdpp_begin(cfg)
+    b.ccdpp_iterate(2)
+    assert a.model() == b.model()
+    assert a.metrics()[0] == b.metrics()[0]
+    b.als_begin(pmf.AlsConfig(k=5, lam=0.05, outer_iters=1, seed=2))
+    b.als_iterate(1)
+    a.als_begin(pmf.AlsConfig(k=5, lam=0.05, outer_iters=1, seed=2))
+    a.als_iterate(1)
+    assert a.model() == b.model()
+    a.close()
+    b.close()
