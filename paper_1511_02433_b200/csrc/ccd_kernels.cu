@@ -19,6 +19,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "device.hpp"
 
@@ -26,7 +27,31 @@ namespace pmfgpu {
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kDefaultPlainVariant = 2;
+constexpr int kDefaultPromoteVariant = 0;
+
+// Launch variants (threads per CTA, unroll of the long / medium / short length classes).  More
+// resident warps keep more loads in flight (scripts/micro/stream_bw.cu: 8 warps/SM cap at ~4 TB/s,
+// 16 at ~6.5, 32 at ~6.9); larger unrolls need more registers.  PMF_SWEEP_VARIANT overrides the
+// default for tuning.
+template <int V>
+struct Var;
+template <>
+struct Var<0> {
+    static constexpr int NT = 512, UA = 8, UB = 4, UC = 4;
+};
+template <>
+struct Var<1> {
+    static constexpr int NT = 1024, UA = 4, UB = 2, UC = 2;
+};
+template <>
+struct Var<2> {
+    static constexpr int NT = 1024, UA = 2, UB = 2, UC = 2;
+};
+template <>
+struct Var<3> {
+    static constexpr int NT = 768, UA = 4, UB = 4, UC = 2;
+};
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -194,8 +219,8 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
     }
 }
 
-template <int MODE, bool CSR, bool IDX16, bool SMEM>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int MODE, bool CSR, bool IDX16, bool SMEM, int V>
+__global__ void __launch_bounds__(Var<V>::NT, 1)
 sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
              const int32_t* __restrict__ piece_start, const int32_t* __restrict__ panel_base,
              const void* __restrict__ idx, float* __restrict__ R, float2* __restrict__ partial,
@@ -249,9 +274,9 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
         const float* g0 = SMEM ? s0 : (MODE == kPlain ? op.gn : op.ga);
         const float* g1 = SMEM ? s1 : op.gb;
         const float* g2 = SMEM ? s2 : op.gn;
-        run_class<MODE, CSR, IDX16, 8, 8>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
-        run_class<MODE, CSR, IDX16, 4, 4>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
-        run_class<MODE, CSR, IDX16, 2, 4>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
+        run_class<MODE, CSR, IDX16, 8, Var<V>::UA>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
+        run_class<MODE, CSR, IDX16, 4, Var<V>::UB>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
+        run_class<MODE, CSR, IDX16, 2, Var<V>::UC>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
     }
     if (op.cta_clock) {
         __syncthreads();
@@ -290,35 +315,54 @@ __global__ void finalize_kernel(const int32_t* __restrict__ mo_out, const int32_
     }
 }
 
-template <int MODE, bool CSR, bool IDX16, bool SMEM>
+template <int MODE, bool CSR, bool IDX16, bool SMEM, int V>
 void launch_one(const DevSweep& L, const SweepOperands& op, size_t smem, cudaStream_t s) {
-    sweep_kernel<MODE, CSR, IDX16, SMEM><<<L.ctas, kThreads, smem, s>>>(
+    sweep_kernel<MODE, CSR, IDX16, SMEM, V><<<L.ctas, Var<V>::NT, smem, s>>>(
         L.units, L.pieces, L.piece_start, L.panel_base, L.idx, L.R, L.partial, op, L.panel_size);
+}
+
+int variant_for(int mode) {
+    static const int plain = [] {
+        const char* e = std::getenv("PMF_SWEEP_VARIANT");
+        return e ? std::atoi(e) : kDefaultPlainVariant;
+    }();
+    static const int promote = [] {
+        const char* e = std::getenv("PMF_PROMOTE_VARIANT");
+        return e ? std::atoi(e) : kDefaultPromoteVariant;
+    }();
+    return mode == kPlain ? plain : promote;
 }
 
 template <int MODE, bool CSR>
 void dispatch_idx(const DevSweep& L, const SweepOperands& op, size_t smem, cudaStream_t s) {
-    if (L.idx16) {
-        if (L.smem) launch_one<MODE, CSR, true, true>(L, op, smem, s);
-        else launch_one<MODE, CSR, true, false>(L, op, smem, s);
-    } else {
-        if (L.smem) launch_one<MODE, CSR, false, true>(L, op, smem, s);
-        else launch_one<MODE, CSR, false, false>(L, op, smem, s);
+    if (L.idx16 && L.smem) {
+        switch (variant_for(MODE)) {
+            case 1: launch_one<MODE, CSR, true, true, 1>(L, op, smem, s); return;
+            case 2: launch_one<MODE, CSR, true, true, 2>(L, op, smem, s); return;
+            case 3: launch_one<MODE, CSR, true, true, 3>(L, op, smem, s); return;
+            default: launch_one<MODE, CSR, true, true, 0>(L, op, smem, s); return;
+        }
     }
+    if (L.idx16) launch_one<MODE, CSR, true, false, 0>(L, op, smem, s);
+    else if (L.smem) launch_one<MODE, CSR, false, true, 0>(L, op, smem, s);
+    else launch_one<MODE, CSR, false, false, 0>(L, op, smem, s);
 }
 
-template <int MODE, bool CSR, bool IDX16, bool SMEM>
+template <int MODE, bool CSR, bool IDX16, bool SMEM, int V>
 void set_attr(size_t max_smem) {
-    cudaFuncSetAttribute(sweep_kernel<MODE, CSR, IDX16, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sweep_kernel<MODE, CSR, IDX16, SMEM, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(max_smem));
 }
 
 template <int MODE, bool CSR>
 void set_attr_all(size_t max_smem) {
-    set_attr<MODE, CSR, true, true>(max_smem);
-    set_attr<MODE, CSR, true, false>(max_smem);
-    set_attr<MODE, CSR, false, true>(max_smem);
-    set_attr<MODE, CSR, false, false>(max_smem);
+    set_attr<MODE, CSR, true, true, 0>(max_smem);
+    set_attr<MODE, CSR, true, true, 1>(max_smem);
+    set_attr<MODE, CSR, true, true, 2>(max_smem);
+    set_attr<MODE, CSR, true, true, 3>(max_smem);
+    set_attr<MODE, CSR, true, false, 0>(max_smem);
+    set_attr<MODE, CSR, false, true, 0>(max_smem);
+    set_attr<MODE, CSR, false, false, 0>(max_smem);
 }
 
 }  // namespace

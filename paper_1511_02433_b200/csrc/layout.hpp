@@ -19,7 +19,7 @@
 namespace pmfgpu {
 
 constexpr int kUnitMax = 1024;      // entries per warp work unit (multiple of 128)
-constexpr int kUnitOverhead = 8;       // cost model: fixed per-unit overhead in "entries"
+constexpr int kUnitOverhead = 20;      // cost model: per-unit overhead in "entries" (fit from per-CTA timings)
 
 // 16-byte work unit, read with one 128-bit load.
 struct Unit {

@@ -215,3 +215,19 @@ def test_distributed_context_single_rank_nccl(pmf, ml100k):
     assert a.model() == b.model()
     a.close()
     b.close()
+
+
+@pytest.mark.slow
+def test_global_gather_layout_vs_oracle(pmf, oracle):
+    """Many short rows over a wide item space (Yahoo-like sparsity): both sides fall back to the
+    non-panel layout that gathers the factor vectors from global memory with 32-bit indices."""
+    m, n = 40000, 70000
+    t = oracle.random_triplets(m, n, 400000, 5)
+    A = pmf.RatingsMatrix.from_triplets(t, m, n)
+    O = oracle.from_triplets(t, m, n)
+    cfg = pmf.CcdConfig(k=4, lam=0.05, outer_iters=2, inner_iters=3, seed=8)
+    model, rep = pmf.ccdpp_train(cfg, A)
+    W, H, rows, _, _ = oracle.ccdpp_train(O, 4, 0.05, 2, 3, 8)
+    for r, g in zip(rep.rows, rows):
+        assert rel(r.objective, g["objective"]) < 1e-4
+    assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
