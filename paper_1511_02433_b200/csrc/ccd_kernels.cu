@@ -27,7 +27,8 @@ namespace pmfgpu {
 
 namespace {
 
-constexpr int kDefaultPlainVariant = 2;
+constexpr int kDefaultPlainVariantCsr = 1;  // u-sweep: 1024 threads, unroll 4/2/2
+constexpr int kDefaultPlainVariantCsc = 2;  // v-sweep: 1024 threads, unroll 2/2/2
 constexpr int kDefaultPromoteVariant = 0;
 
 // Launch variants (threads per CTA, unroll of the long / medium / short length classes).  More
@@ -321,11 +322,12 @@ void launch_one(const DevSweep& L, const SweepOperands& op, size_t smem, cudaStr
         L.units, L.pieces, L.piece_start, L.panel_base, L.idx, L.R, L.partial, op, L.panel_size);
 }
 
-int variant_for(int mode) {
+int variant_for(int mode, bool csr) {
     static const int plain = [] {
         const char* e = std::getenv("PMF_SWEEP_VARIANT");
-        return e ? std::atoi(e) : kDefaultPlainVariant;
+        return e ? std::atoi(e) : -1;
     }();
+    if (mode == kPlain && plain < 0) return csr ? kDefaultPlainVariantCsr : kDefaultPlainVariantCsc;
     static const int promote = [] {
         const char* e = std::getenv("PMF_PROMOTE_VARIANT");
         return e ? std::atoi(e) : kDefaultPromoteVariant;
@@ -336,7 +338,7 @@ int variant_for(int mode) {
 template <int MODE, bool CSR>
 void dispatch_idx(const DevSweep& L, const SweepOperands& op, size_t smem, cudaStream_t s) {
     if (L.idx16 && L.smem) {
-        switch (variant_for(MODE)) {
+        switch (variant_for(MODE, CSR)) {
             case 1: launch_one<MODE, CSR, true, true, 1>(L, op, smem, s); return;
             case 2: launch_one<MODE, CSR, true, true, 2>(L, op, smem, s); return;
             case 3: launch_one<MODE, CSR, true, true, 3>(L, op, smem, s); return;

@@ -71,6 +71,33 @@ bool partition_balanced(const int64_t* costs, int32_t count, int p, int32_t* bou
 
 static inline int64_t round4(int64_t x) { return (x + 3) & ~int64_t(3); }
 
+// parallel_for over outputs [0, n_out) with chunks of equal entry counts (start = offsets)
+static void parallel_for_outputs(const int64_t* start, int32_t out_begin, int32_t n_out,
+                                 const std::function<void(int64_t, int64_t)>& fn) {
+    const int T = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+    const int64_t total = start[out_begin + n_out] - start[out_begin];
+    if (T <= 1 || n_out < 2 * T || total < (int64_t(1) << 16)) {
+        fn(0, n_out);
+        return;
+    }
+    const int chunks = 4 * T;
+    std::vector<int64_t> cut(chunks + 1, 0);
+    for (int c = 1; c < chunks; ++c) {
+        const int64_t target = start[out_begin] + total * c / chunks;
+        cut[c] = std::lower_bound(start + out_begin, start + out_begin + n_out, target) - (start + out_begin);
+        cut[c] = std::max(cut[c], cut[c - 1]);
+    }
+    cut[chunks] = n_out;
+    std::atomic<int> next{0};
+    std::vector<std::thread> ts;
+    for (int t = 0; t < T; ++t)
+        ts.emplace_back([&] {
+            for (int c; (c = next++) < chunks;)
+                if (cut[c] < cut[c + 1]) fn(cut[c], cut[c + 1]);
+        });
+    for (auto& t : ts) t.join();
+}
+
 SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const float* val,
                                int32_t out_begin, int32_t out_end, const int32_t* gmap,
                                int32_t gat_extent, int stage_arrays, int smem_budget_bytes,
@@ -88,40 +115,49 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     if (allow_idx16) pg_cap = std::min<int64_t>(pg_cap, 65532);
     const int64_t nnz_side = start[out_end] - start[out_begin];
     L.n_real = nnz_side;
+    // panel of gather index g, tracked incrementally along an output's ascending indices
+    auto count_segments = [&](int32_t pg, int32_t np, std::vector<int32_t>& seg_len) {
+        seg_len.assign(static_cast<size_t>(np) * n_out, 0);
+        parallel_for_outputs(start, out_begin, n_out, [&](int64_t ob, int64_t oe) {
+            for (int64_t o = ob; o < oe; ++o) {
+                int32_t p = 0;
+                int64_t bound = pg;  // first gather index of panel p+1
+                for (int64_t e = start[out_begin + o]; e < start[out_begin + o + 1]; ++e) {
+                    const int32_t g = gidx(e);
+                    while (g >= bound) {
+                        ++p;
+                        bound += pg;
+                    }
+                    seg_len[static_cast<size_t>(p) * n_out + o]++;
+                }
+            }
+        });
+    };
+    std::vector<int32_t> seg_len;
     if (gat_extent <= pg_cap) {
         L.smem = true;
         L.panel_size = std::max(gat_extent, 1);
         L.n_panels = 1;
         L.idx16 = allow_idx16 && gat_extent <= 65535;
+        count_segments(L.panel_size, 1, seg_len);
     } else {
         const int32_t pg = static_cast<int32_t>(pg_cap);
         const int32_t np = static_cast<int32_t>((static_cast<int64_t>(gat_extent) + pg - 1) / pg);
-        std::atomic<int64_t> segs{0};
-        parallel_for(n_out, [&](int64_t ob, int64_t oe) {
-            int64_t local = 0;
-            for (int64_t o = ob; o < oe; ++o) {
-                int32_t last = -1;
-                for (int64_t e = start[out_begin + o]; e < start[out_begin + o + 1]; ++e) {
-                    const int32_t p = gidx(e) / pg;
-                    if (p != last) {
-                        ++local;
-                        last = p;
-                    }
-                }
-            }
-            segs += local;
-        });
-        const double avg = segs.load() ? static_cast<double>(nnz_side) / segs.load() : 0.0;
+        count_segments(pg, np, seg_len);
+        int64_t segs = 0;
+        for (auto x : seg_len) segs += x > 0;
+        const double avg = segs ? static_cast<double>(nnz_side) / segs : 0.0;
         if (avg >= 48.0) {
             L.smem = true;
             L.panel_size = pg;
             L.n_panels = np;
             L.idx16 = allow_idx16;
-        } else {
+        } else {  // segments too short for panels: gather from global memory, 32-bit indices
             L.smem = false;
             L.panel_size = gat_extent;
             L.n_panels = 1;
             L.idx16 = false;
+            count_segments(std::max(gat_extent, 1), 1, seg_len);
         }
     }
     L.sentinel = L.smem ? L.panel_size : gat_extent;
@@ -132,15 +168,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     const int32_t pg = L.panel_size;
     const int32_t np = L.n_panels;
 
-    // ---- 2. segment lengths (panel-major) --------------------------------------------------
-    std::vector<int32_t> seg_len(static_cast<size_t>(np) * n_out, 0);
-    parallel_for(n_out, [&](int64_t ob, int64_t oe) {
-        for (int64_t o = ob; o < oe; ++o)
-            for (int64_t e = start[out_begin + o]; e < start[out_begin + o + 1]; ++e) {
-                const int32_t p = np == 1 ? 0 : gidx(e) / pg;
-                seg_len[static_cast<size_t>(p) * n_out + o]++;
-            }
-    });
+    // ---- 2. segment offsets (panel-major) ----------------------------------------------------
     std::vector<int64_t> seg_off(seg_len.size() + 1, 0);
     int64_t nonempty = 0;
     for (size_t s = 0; s < seg_len.size(); ++s) {
@@ -151,20 +179,35 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     L.avg_segment = nonempty ? static_cast<double>(nnz_side) / nonempty : 0.0;
     if (L.n_entries >= (int64_t(1) << 32)) throw std::length_error("too many entries for 32-bit units");
 
-    // ---- 3. fill entries ---------------------------------------------------------------------
-    if (L.idx16) L.idx16v.assign(L.n_entries, static_cast<uint16_t>(L.sentinel));
-    else L.idx32v.assign(L.n_entries, L.sentinel);
-    L.val.assign(L.n_entries, 0.0f);
-    parallel_for(n_out, [&](int64_t ob, int64_t oe) {
+    // ---- 3. fill entries (padding of each segment written by its owner thread) -----------------
+    if (L.idx16) L.idx16v.alloc(L.n_entries);
+    else L.idx32v.alloc(L.n_entries);
+    L.val.alloc(L.n_entries);
+    parallel_for_outputs(start, out_begin, n_out, [&](int64_t ob, int64_t oe) {
+        auto pad = [&](int64_t w, int64_t end) {
+            for (; w < end; ++w) {
+                if (L.idx16) L.idx16v[w] = static_cast<uint16_t>(L.sentinel);
+                else L.idx32v[w] = L.sentinel;
+                L.val[w] = 0.0f;
+            }
+        };
         for (int64_t o = ob; o < oe; ++o) {
             int32_t cur_p = -1;
-            int64_t w = 0;
+            int64_t w = 0, wend = 0;
+            int32_t p = 0;
+            int64_t bound = pg;
             for (int64_t e = start[out_begin + o]; e < start[out_begin + o + 1]; ++e) {
                 const int32_t g = gidx(e);
-                const int32_t p = np == 1 ? 0 : g / pg;
+                while (np > 1 && g >= bound) {
+                    ++p;
+                    bound += pg;
+                }
                 if (p != cur_p) {
+                    if (cur_p >= 0) pad(w, wend);
                     cur_p = p;
-                    w = seg_off[static_cast<size_t>(p) * n_out + o];
+                    const size_t sidx = static_cast<size_t>(p) * n_out + o;
+                    w = seg_off[sidx];
+                    wend = seg_off[sidx + 1];
                 }
                 const int32_t local = g - L.panel_base[p];
                 if (L.idx16) L.idx16v[w] = static_cast<uint16_t>(local);
@@ -172,6 +215,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
                 L.val[w] = val[e];
                 ++w;
             }
+            if (cur_p >= 0) pad(w, wend);
         }
     });
 

@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <functional>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -20,6 +21,28 @@ namespace pmfgpu {
 
 constexpr int kUnitMax = 1024;      // entries per warp work unit (multiple of 128)
 constexpr int kUnitOverhead = 20;      // cost model: per-unit overhead in "entries" (fit from per-CTA timings)
+
+// Uninitialised POD buffer (large layout arrays are filled in parallel; std::vector would first
+// value-initialise them serially).
+template <class T>
+struct PodBuf {
+    std::unique_ptr<T[]> p;
+    size_t n = 0;
+    void alloc(size_t count) {
+        p.reset(new T[count ? count : 1]);
+        n = count;
+    }
+    void reset() {
+        p.reset();
+        n = 0;
+    }
+    T* data() { return p.get(); }
+    const T* data() const { return p.get(); }
+    size_t size() const { return n; }
+    bool empty() const { return n == 0; }
+    T& operator[](size_t i) { return p[i]; }
+    const T& operator[](size_t i) const { return p[i]; }
+};
 
 // 16-byte work unit, read with one 128-bit load.
 struct Unit {
@@ -52,9 +75,9 @@ struct SweepLayout {
     std::vector<int32_t> panel_base;  // n_panels + 1
     int64_t n_entries = 0;            // padded entry count (multiple of 4)
     int64_t n_real = 0;
-    std::vector<uint16_t> idx16v;
-    std::vector<int32_t> idx32v;
-    std::vector<float> val;           // padded values (A), padding = 0
+    PodBuf<uint16_t> idx16v;
+    PodBuf<int32_t> idx32v;
+    PodBuf<float> val;                // padded values (A), padding = 0
     std::vector<Unit> units;
     std::vector<int32_t> unit_panel;
     std::vector<int32_t> unit_real;   // real (unpadded) entries of each unit

@@ -11,6 +11,8 @@
 #include <chrono>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <random>
@@ -83,6 +85,13 @@ struct DevMem {
     }
     template <class T>
     T* upload(const std::vector<T>& v, cudaStream_t s, int64_t* h2d) {
+        T* p = alloc<T>(v.size(), false);
+        if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (h2d) *h2d += static_cast<int64_t>(v.size() * sizeof(T));
+        return p;
+    }
+    template <class T>
+    T* upload(const PodBuf<T>& v, cudaStream_t s, int64_t* h2d) {
         T* p = alloc<T>(v.size(), false);
         if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
         if (h2d) *h2d += static_cast<int64_t>(v.size() * sizeof(T));
@@ -211,9 +220,9 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     D.partial = c.mem.alloc<float2>(std::max(1, L.n_slots));
     CUDA_TRY(cudaStreamSynchronize(c.stream));
     // keep only the metadata needed for residual readback
-    std::vector<uint16_t>().swap(L.idx16v);
-    std::vector<int32_t>().swap(L.idx32v);
-    std::vector<float>().swap(L.val);
+    L.idx16v.reset();
+    L.idx32v.reset();
+    L.val.reset();
     return D;
 }
 
@@ -278,6 +287,7 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     }
     const int32_t* rmap = c->rmap.empty() ? nullptr : c->rmap.data();
     const int32_t* cmap = c->cmap.empty() ? nullptr : c->cmap.data();
+    const double t_layout = now_s();
     c->hcsr = build_sweep_layout(a->row_start, a->col_of, a->val_row, c->row_begin, c->row_end, cmap, c->ext_n,
                                  2, kSmemBudget, c->sm_count);
     c->hcsc = build_sweep_layout(a->col_start, a->row_of, a->val_col, c->col_begin, c->col_end, rmap, c->ext_m,
@@ -292,14 +302,19 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
         als_set_attributes();
         attrs_set = true;
     }
+    const double t_upload = now_s();
     c->csr = upload_sweep(*c, c->hcsr, &c->A_csr);
     c->csc = upload_sweep(*c, c->hcsc, &c->A_csc);
+    const double t_done = now_s();
     // eval scratch
     c->unit_loss = c->eval_mem.alloc<double>(std::max(c->csr.n_units, 1));
     c->red_scratch = c->eval_mem.alloc<double>(4096);
     c->red_out = c->eval_mem.alloc<double>(8);
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->setup_seconds = now_s() - t0;
+    if (std::getenv("PMF_VERBOSE"))
+        std::fprintf(stderr, "[pmf] ctx setup %.3f s: device init %.3f, layouts %.3f, upload %.3f, rest %.3f\n",
+                     c->setup_seconds, t_layout - t0, t_upload - t_layout, t_done - t_upload, now_s() - t_done);
     return c;
 }
 
