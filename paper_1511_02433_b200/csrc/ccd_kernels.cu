@@ -117,7 +117,7 @@ template <int MODE, bool CSR>
 struct Roles {
     // staged arrays: plain: s0 = gn;  promote CSR: s0 = ga, s1 = gb (gn == gb);
     // promote CSC: s0 = ga, s1 = gb, s2 = gn;  demote: s0 = ga.
-    static constexpr int kArrays = MODE == kPromote ? (CSR ? 2 : 3) : 1;
+    static constexpr int kArrays = MODE == kPromote ? (CSR ? 2 : 3) : MODE == kRmw ? 2 : 1;
 };
 
 __host__ __device__ __forceinline__ int stage_stride(int panel_size) { return ((panel_size + 1) + 3) & ~3; }
@@ -149,7 +149,7 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
         const int32_t oidx = op.out_off + U.o;
         float oa = 0.f, ob = 0.f;
         if (MODE != kPlain && U.len > 0) oa = __ldg(op.oa + oidx);
-        if (MODE == kPromote && U.len > 0) ob = __ldg(op.ob + oidx);
+        if ((MODE == kPromote || MODE == kRmw) && U.len > 0) ob = __ldg(op.ob + oidx);
         const int64_t end = static_cast<int64_t>(U.e0) + U.len;
         const int my_steps = (U.len + 4 * G * kUnroll - 1) / (4 * G * kUnroll);
         const int steps = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_steps)));
@@ -184,6 +184,13 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
                             den = fmaf(gv, gv, den);
                         } else if (MODE == kDemote) {
                             r = __fsub_rn(r, __fmul_rn(oa, g0[gi]));
+                        } else if (MODE == kRmw) {
+                            const float a = g0[gi];
+                            const float b = g1[gi];
+                            r = __fsub_rn(r, __fmul_rn(oa, a));
+                            const float w = CSR ? ob : b;
+                            const float h = CSR ? b : ob;
+                            if (w != 0.f) r = __fadd_rn(r, __fmul_rn(w, h));
                         } else {
                             const float a = g0[gi];
                             const float b = g1[gi];
@@ -203,7 +210,7 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
                 }
             }
         }
-        if (MODE == kDemote) continue;
+        if (MODE == kDemote || MODE == kRmw) continue;
 #pragma unroll
         for (int off = G / 2; off > 0; off >>= 1) {
             num += __shfl_xor_sync(0xffffffffu, num, off);
@@ -332,6 +339,11 @@ int variant_for(int mode, bool csr) {
         const char* e = std::getenv("PMF_PROMOTE_VARIANT");
         return e ? std::atoi(e) : kDefaultPromoteVariant;
     }();
+    static const int rmw = [] {
+        const char* e = std::getenv("PMF_RMW_VARIANT");
+        return e ? std::atoi(e) : 2;
+    }();
+    if (mode == kRmw) return rmw;
     return mode == kPlain ? plain : promote;
 }
 
@@ -371,7 +383,7 @@ void set_attr_all(size_t max_smem) {
 
 size_t sweep_smem_bytes(const DevSweep& L, SweepMode mode, bool csr_side) {
     if (!L.smem) return 0;
-    const int arrays = mode == kPromote ? (csr_side ? 2 : 3) : 1;
+    const int arrays = mode == kPromote ? (csr_side ? 2 : 3) : mode == kRmw ? 2 : 1;
     return static_cast<size_t>(arrays) * stage_stride(L.panel_size) * sizeof(float);
 }
 
@@ -382,6 +394,8 @@ void sweep_set_attributes(size_t max_smem) {
     set_attr_all<kPromote, false>(max_smem);
     set_attr_all<kDemote, true>(max_smem);
     set_attr_all<kDemote, false>(max_smem);
+    set_attr_all<kRmw, true>(max_smem);
+    set_attr_all<kRmw, false>(max_smem);
 }
 
 int launch_sweep(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOperands& op,
@@ -395,13 +409,16 @@ int launch_sweep(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOp
         } else if (mode == kPromote) {
             if (csr_side) dispatch_idx<kPromote, true>(L, op, smem, stream);
             else dispatch_idx<kPromote, false>(L, op, smem, stream);
+        } else if (mode == kRmw) {
+            if (csr_side) dispatch_idx<kRmw, true>(L, op, smem, stream);
+            else dispatch_idx<kRmw, false>(L, op, smem, stream);
         } else {
             if (csr_side) dispatch_idx<kDemote, true>(L, op, smem, stream);
             else dispatch_idx<kDemote, false>(L, op, smem, stream);
         }
         ++launched;
     }
-    if (mode != kDemote && L.n_mo > 0) {
+    if (mode != kDemote && mode != kRmw && L.n_mo > 0) {
         const int threads = 256;
         const int64_t warps = L.n_mo;
         const int blocks = static_cast<int>(std::min<int64_t>((warps * 32 + threads - 1) / threads, 4096));

@@ -27,7 +27,8 @@ struct DevSweep {
     float2* partial = nullptr;
 };
 
-enum SweepMode { kPlain = 0, kPromote = 1, kDemote = 2 };
+// kRmw: the promote's residual update alone (R <- (R - u'v') + [w != 0] w h), no accumulation
+enum SweepMode { kPlain = 0, kPromote = 1, kDemote = 2, kRmw = 3 };
 
 // Operands of one sweep.  "g*" vectors are indexed by the gather index (padded space),
 // "o*" vectors by the output index (out_off + local output).

@@ -411,6 +411,16 @@ struct SweepTimer {
     }
 };
 
+// First sweep of a step: fused promote kernel, or a separate residual pass + plain sweep
+// (PMF_SPLIT_PROMOTE = bitmask: 1 = CSR side, 2 = CSC side).
+bool split_promote(bool csr) {
+    static const int mask = [] {
+        const char* e = std::getenv("PMF_SPLIT_PROMOTE");
+        return e ? std::atoi(e) : 0;
+    }();
+    return (mask & (csr ? 1 : 2)) != 0;
+}
+
 // Enqueues one CCD++ outer iteration (ccd.hpp:373-393) on c.stream; returns kernels launched.
 int64_t enqueue_ccd_iteration(Ctx& c) {
     int64_t launched = 0;
@@ -437,7 +447,14 @@ int64_t enqueue_ccd_iteration(Ctx& c) {
                 ou.gn = c.vbuf;
             }
             tm.start();
-            launched += launch_sweep(c.csr, s == 0 ? kPromote : kPlain, true, ou, c.stream);
+            if (s == 0 && split_promote(true)) {
+                launched += launch_sweep(c.csr, kRmw, true, ou, c.stream);
+                SweepOperands up = ou;
+                up.gn = Ht;
+                launched += launch_sweep(c.csr, kPlain, true, up, c.stream);
+            } else {
+                launched += launch_sweep(c.csr, s == 0 ? kPromote : kPlain, true, ou, c.stream);
+            }
             tm.stop(true);
             allgather(c, c.ubuf, c.Bm);
             SweepOperands ov;
@@ -452,7 +469,13 @@ int64_t enqueue_ccd_iteration(Ctx& c) {
                 ov.ob = Ht;  // h
             }
             tm.start();
-            launched += launch_sweep(c.csc, s == 0 ? kPromote : kPlain, false, ov, c.stream);
+            if (s == 0 && split_promote(false)) {
+                // residual update as its own streaming pass, then a plain sweep
+                launched += launch_sweep(c.csc, kRmw, false, ov, c.stream);
+                launched += launch_sweep(c.csc, kPlain, false, ov, c.stream);
+            } else {
+                launched += launch_sweep(c.csc, s == 0 ? kPromote : kPlain, false, ov, c.stream);
+            }
             tm.stop(false);
             allgather(c, c.vbuf, c.Bn);
         }
