@@ -160,7 +160,8 @@ pmf_status pmf_ctx_kernel_stats(pmf_ctx* ctx, double* usweep_ms, int64_t* usweep
 pmf_status pmf_ctx_launch_count(pmf_ctx* ctx, int64_t* per_iteration);
 /* Diagnostic: runs one sweep (side 0 = u over CSR, 1 = v over CSC; promote or plain) on a copy of the
  * residual and returns per-CTA [start, end] globaltimer ns (2*ctas) and per-CTA layout stats
- * (6*ctas: long/medium/short units, entries, pieces, last panel). */
+ * (24*ctas: long/medium/short units, entries, pieces, last panel, entries per class, then for unroll
+ * 1/2/4/8 the per-class sums of ceil(len / (4 * lanes * unroll)) group-steps; rest 0). */
 pmf_status pmf_ctx_debug_sweep_profile(pmf_ctx* ctx, int32_t side, int32_t promote, uint64_t* cta_ns,
                                       int64_t* cta_stats, int32_t* n_ctas);
 /* Enables (1) / disables (0) per-sweep CUDA-event timing inside pmf_ctx_ccdpp_iterate. */

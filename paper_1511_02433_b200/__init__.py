@@ -674,10 +674,10 @@ class Context:
 
     def debug_sweep_profile(self, side: int, promote: bool = False):
         n = C.c_int32()
-        clk = np.zeros(2 * 1024, np.uint64); st = np.zeros(6 * 1024, np.int64)
+        clk = np.zeros(2 * 1024, np.uint64); st = np.zeros(24 * 1024, np.int64)
         _check(lib.pmf_ctx_debug_sweep_profile(self.h, side, 1 if promote else 0, _ptr(clk), _ptr(st), C.byref(n)))
         c = n.value
-        return clk[:2 * c].reshape(c, 2), st[:6 * c].reshape(c, 6)
+        return clk[:2 * c].reshape(c, 2), st[:24 * c].reshape(c, 24)
 
     def launch_count(self) -> int:
         n = C.c_int64()

@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
+#include <cstdlib>
 #include <numeric>
 #include <stdexcept>
 #include <thread>
@@ -24,6 +26,33 @@ void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn, in
         ts.emplace_back([&fn, b, e] { fn(b, e); });
     }
     for (auto& t : ts) t.join();
+}
+
+UnitCost unit_cost_model() {
+    UnitCost m;
+    // PMF_UNIT_COST = 19 integers in UnitCost field order (experiments only)
+    if (const char* e = std::getenv("PMF_UNIT_COST")) {
+        int64_t v[19];
+        int n = 0;
+        for (const char* p = e; n < 19 && *p;) {
+            char* q;
+            const int64_t x = std::strtoll(p, &q, 10);
+            if (q == p) break;
+            v[n++] = x;
+            p = *q == ',' ? q + 1 : q;
+        }
+        if (n == 19)
+            for (int c = 0; c < 3; ++c) {
+                m.step_a[c] = std::max<int64_t>(1, v[c]);
+                m.per_step_a[c] = v[3 + c];
+                m.step_b[c] = std::max<int64_t>(1, v[6 + c]);
+                m.per_step_b[c] = v[9 + c];
+                m.per_entry[c] = v[12 + c];
+                m.per_unit[c] = v[15 + c];
+                m.per_piece = v[18];
+            }
+    }
+    return m;
 }
 
 bool partition_balanced(const int64_t* costs, int32_t count, int p, int32_t* bounds) {
@@ -254,8 +283,15 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
 
     // ---- 5. per-CTA pieces: contiguous unit ranges of equal cost, split at panel changes -----
     const int64_t nu = static_cast<int64_t>(L.units.size());
+    const UnitCost cm = unit_cost_model();
     std::vector<int64_t> pre(nu + 1, 0);
-    for (int64_t u = 0; u < nu; ++u) pre[u + 1] = pre[u] + L.units[u].len + kUnitOverhead;
+    for (int64_t u = 0; u < nu; ++u) {
+        const int64_t len = L.units[u].len;
+        const int c = len > kMidLen ? 0 : len > kShortLen ? 1 : 2;
+        pre[u + 1] = pre[u] + (len + cm.step_a[c] - 1) / cm.step_a[c] * cm.per_step_a[c] +
+                     (len + cm.step_b[c] - 1) / cm.step_b[c] * cm.per_step_b[c] + len * cm.per_entry[c] +
+                     cm.per_unit[c] + (u > 0 && L.unit_panel[u] != L.unit_panel[u - 1] ? cm.per_piece : 0);
+    }
     L.piece_start.assign(ctas + 1, 0);
     int64_t ub = 0;
     for (int c = 0; c < ctas; ++c) {

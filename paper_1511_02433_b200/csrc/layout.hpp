@@ -20,7 +20,23 @@
 namespace pmfgpu {
 
 constexpr int kUnitMax = 1024;      // entries per warp work unit (multiple of 128)
-constexpr int kUnitOverhead = 20;      // cost model: per-unit overhead in "entries" (fit from per-CTA timings)
+// Cost model of the CTA partition, in picoseconds of CTA time, fitted by regression on per-CTA sweep
+// timings under several partitions (scripts/cta_fit.py over pmf_ctx_debug_sweep_profile, Netflix
+// shape).  One layout serves the 14 plain sweeps and the promote sweep of a rank-one step, so the
+// model is 14 x plain + 1 x promote.  Per length class (long / medium / short): a cost per group-step
+// of each kernel (a warp batch pays for its steps whatever their fill; plain steps 64/32/16 entries,
+// promote 256/64/32), per entry and per unit; plus a cost per piece (panel staging and the barrier
+// that drains the CTA before the next panel).
+struct UnitCost {
+    int64_t step_a[3] = {64, 32, 16};
+    int64_t per_step_a[3] = {34552, 54236, 0};
+    int64_t step_b[3] = {256, 64, 32};
+    int64_t per_step_b[3] = {11776, 11471, 0};
+    int64_t per_entry[3] = {1235, 203, 2878};
+    int64_t per_unit[3] = {63621, 5735, 5628};
+    int64_t per_piece = 109820213;
+};
+UnitCost unit_cost_model();
 
 // Uninitialised POD buffer (large layout arrays are filled in parallel; std::vector would first
 // value-initialise them serially).

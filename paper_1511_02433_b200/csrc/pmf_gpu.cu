@@ -914,15 +914,26 @@ pmf_status pmf_ctx_debug_sweep_profile(pmf_ctx* ctx, int32_t side, int32_t promo
         CUDA_TRY(cudaStreamSynchronize(c.stream));
         CUDA_TRY(cudaMemcpy(cta_ns, clk, sizeof(uint64_t) * 2 * L.ctas, cudaMemcpyDeviceToHost));
         if (cta_stats) {
-            for (int x = 0; x < 6 * L.ctas; ++x) cta_stats[x] = 0;
+            constexpr int W = 24;
+            for (int x = 0; x < W * L.ctas; ++x) cta_stats[x] = 0;
             for (int cc = 0; cc < L.ctas; ++cc)
                 for (int p = H.piece_start[cc]; p < H.piece_start[cc + 1]; ++p) {
                     const Piece& pz = H.pieces[p];
-                    int64_t* st = cta_stats + 6 * cc;
+                    int64_t* st = cta_stats + W * cc;
                     st[0] += pz.um - pz.ub;
                     st[1] += pz.us - pz.um;
                     st[2] += pz.ue - pz.us;
-                    for (int u = pz.ub; u < pz.ue; ++u) st[3] += H.units[u].len;
+                    for (int u = pz.ub; u < pz.ue; ++u) {
+                        const int len = H.units[u].len;
+                        const int cls = u < pz.um ? 0 : u < pz.us ? 1 : 2;
+                        const int g = 8 >> cls;
+                        st[3] += len;
+                        st[6 + cls] += len;
+                        for (int j = 0; j < 4; ++j) {
+                            const int step = 4 * g << j;
+                            st[9 + 3 * j + cls] += (len + step - 1) / step;
+                        }
+                    }
                     st[4] += 1;
                     st[5] = pz.panel;
                 }
