@@ -53,6 +53,22 @@ template <>
 struct Var<3> {
     static constexpr int NT = 768, UA = 4, UB = 4, UC = 2;
 };
+// Software-pipelined plain sweeps (run_class_pipe): the next step's loads are in flight while the
+// current step is reduced, so each lane needs half the unroll for the same bytes in flight.
+template <>
+struct Var<4> {
+    static constexpr int NT = 1024, UA = 2, UB = 2, UC = 1;
+};
+template <>
+struct Var<5> {
+    static constexpr int NT = 1024, UA = 2, UB = 1, UC = 1;
+};
+template <>
+struct Var<6> {
+    static constexpr int NT = 512, UA = 4, UB = 4, UC = 2;
+};
+template <int V>
+constexpr bool kPipelined = V >= 4;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -227,6 +243,137 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
     }
 }
 
+// Plain-sweep variant of run_class with the loads software-pipelined across steps and unit
+// batches: a warp walks the flattened sequence of (batch, step) pairs and issues the loads of the
+// next pair before gathering and accumulating the current one, so its loads are in flight
+// continuously instead of only between batches.  Same per-unit arithmetic and reduction order as
+// run_class (bitwise identical results).
+template <bool IDX16, int G, int kUnroll>
+struct PipeBuf {
+    float4 r[kUnroll];
+    typename IdxVec<IDX16>::raw_t ix[kUnroll];
+    int rem;
+};
+
+template <bool IDX16, int G, int kUnroll>
+__device__ __forceinline__ void pipe_load(PipeBuf<IDX16, G, kUnroll>& b, const Unit& U, int s, int gl,
+                                          const void* __restrict__ idx, const float* __restrict__ R) {
+    const int64_t base = static_cast<int64_t>(U.e0) + 4 * (gl + G * kUnroll * s);
+    b.rem = static_cast<int>(static_cast<int64_t>(U.e0) + U.len - base);
+    const float4* rp = reinterpret_cast<const float4*>(R + base);
+    const typename IdxVec<IDX16>::raw_t* ip = reinterpret_cast<const typename IdxVec<IDX16>::raw_t*>(
+        static_cast<const char*>(idx) + base * (IDX16 ? 2 : 4));
+    // every register of the buffer is redefined (zero past the end), so no value of the previous
+    // stage stays live across the loop
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q) {
+        const bool in = 4 * G * q < b.rem;
+        b.r[q] = in ? __ldcs(rp + G * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        b.ix[q] = in ? __ldcs(ip + G * q) : typename IdxVec<IDX16>::raw_t{};
+    }
+}
+
+template <bool IDX16, int G, int kUnroll>
+__device__ __forceinline__ void pipe_accumulate(const PipeBuf<IDX16, G, kUnroll>& b, const float* g0, float& num,
+                                                float& den) {
+    using IV = IdxVec<IDX16>;
+#pragma unroll
+    for (int q = 0; q < kUnroll; ++q)
+        if (4 * G * q < b.rem) {
+            const float rv[4] = {b.r[q].x, b.r[q].y, b.r[q].z, b.r[q].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const float gv = g0[IV::get(b.ix[q], c)];
+                num = fmaf(rv[c], gv, num);
+                den = fmaf(gv, gv, den);
+            }
+        }
+}
+
+// State of one warp's walk over its (batch, step) sequence.
+struct PipeState {
+    Unit U, Un;    // current batch's unit (per group) and the next batch's (prefetched)
+    int nbn;       // first unit index of the next batch
+    int steps, s;  // group-steps of the current batch (warp maximum) and the current step
+    float num, den;
+};
+
+template <bool IDX16, int G, int kUnroll>
+__device__ __forceinline__ void pipe_grab(int* counter, int32_t ue, const Unit* __restrict__ units, int& nb,
+                                          Unit& u) {
+    const int lane = threadIdx.x & 31;
+    if (lane == 0) nb = atomicAdd(counter, 32 / G);
+    nb = __shfl_sync(0xffffffffu, nb, 0);
+    u = (nb + lane / G < ue) ? units[nb + lane / G] : Unit{0u, 0, 0, -2};
+}
+
+template <int G, int kUnroll>
+__device__ __forceinline__ int pipe_steps(const Unit& u) {
+    constexpr int SE = 4 * G * kUnroll;
+    const int my = (u.len + SE - 1) / SE;
+    return max(1, static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(my))));
+}
+
+// One pipeline stage: prefetch the next (batch, step) into `nx`, consume `cur`.  Returns false when
+// the warp has no further batch.
+template <bool IDX16, int G, int kUnroll>
+__device__ __forceinline__ bool pipe_stage(PipeState& st, PipeBuf<IDX16, G, kUnroll>& cur,
+                                           PipeBuf<IDX16, G, kUnroll>& nx, int* counter, int32_t ue,
+                                           const Unit* __restrict__ units, const void* __restrict__ idx,
+                                           const float* __restrict__ R, float2* __restrict__ partial,
+                                           const SweepOperands& op, const float* g0) {
+    const int gl = (threadIdx.x & 31) % G;
+    const bool adv = st.s + 1 >= st.steps;
+    if (adv) pipe_load(nx, st.Un, 0, gl, idx, R);  // Un.len == 0 past the end: no loads
+    else pipe_load(nx, st.U, st.s + 1, gl, idx, R);
+    pipe_accumulate(cur, g0, st.num, st.den);
+    if (!adv) {
+        ++st.s;
+        return true;
+    }
+    float num = st.num, den = st.den;
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+        num += __shfl_xor_sync(0xffffffffu, num, off);
+        den += __shfl_xor_sync(0xffffffffu, den, off);
+    }
+    if (gl == 0 && st.U.len > 0) {
+        if (st.U.slot < 0) {
+            const float dt = __fadd_rn(op.lambda, den);
+            op.out[op.out_off + st.U.o] = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+        } else {
+            partial[st.U.slot] = make_float2(num, den);
+        }
+    }
+    st.num = st.den = 0.f;
+    if (st.nbn >= ue) return false;
+    st.U = st.Un;
+    st.steps = pipe_steps<G, kUnroll>(st.U);
+    st.s = 0;
+    pipe_grab<IDX16, G, kUnroll>(counter, ue, units, st.nbn, st.Un);
+    return true;
+}
+
+template <bool IDX16, int G, int kUnroll>
+__device__ __forceinline__ void run_class_pipe(int* counter, int32_t ub, int32_t ue, const Unit* __restrict__ units,
+                                            const void* __restrict__ idx, const float* __restrict__ R,
+                                            float2* __restrict__ partial, const SweepOperands& op,
+                                            const float* g0) {
+    if (ub >= ue) return;
+    PipeState st;
+    int nb;
+    pipe_grab<IDX16, G, kUnroll>(counter, ue, units, nb, st.U);
+    if (nb >= ue) return;
+    pipe_grab<IDX16, G, kUnroll>(counter, ue, units, st.nbn, st.Un);
+    st.steps = pipe_steps<G, kUnroll>(st.U);
+    st.s = 0;
+    st.num = st.den = 0.f;
+    PipeBuf<IDX16, G, kUnroll> cur, nx;
+    pipe_load(cur, st.U, 0, (threadIdx.x & 31) % G, idx, R);
+    // the loop-carried buffer is renamed, not copied, once the loop is in SSA form
+    while (pipe_stage(st, cur, nx, counter, ue, units, idx, R, partial, op, g0)) cur = nx;
+}
+
 template <int MODE, bool CSR, bool IDX16, bool SMEM, int V>
 __global__ void __launch_bounds__(Var<V>::NT, 1)
 sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
@@ -282,9 +429,15 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
         const float* g0 = SMEM ? s0 : (MODE == kPlain ? op.gn : op.ga);
         const float* g1 = SMEM ? s1 : op.gb;
         const float* g2 = SMEM ? s2 : op.gn;
-        run_class<MODE, CSR, IDX16, 8, Var<V>::UA>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
-        run_class<MODE, CSR, IDX16, 4, Var<V>::UB>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
-        run_class<MODE, CSR, IDX16, 2, Var<V>::UC>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
+        if constexpr (MODE == kPlain && kPipelined<V>) {
+            run_class_pipe<IDX16, 8, Var<V>::UA>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0);
+            run_class_pipe<IDX16, 4, Var<V>::UB>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0);
+            run_class_pipe<IDX16, 2, Var<V>::UC>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0);
+        } else {
+            run_class<MODE, CSR, IDX16, 8, Var<V>::UA>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
+            run_class<MODE, CSR, IDX16, 4, Var<V>::UB>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
+            run_class<MODE, CSR, IDX16, 2, Var<V>::UC>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
+        }
     }
     if (op.cta_clock) {
         __syncthreads();
@@ -354,8 +507,18 @@ void dispatch_idx(const DevSweep& L, const SweepOperands& op, size_t smem, cudaS
             case 1: launch_one<MODE, CSR, true, true, 1>(L, op, smem, s); return;
             case 2: launch_one<MODE, CSR, true, true, 2>(L, op, smem, s); return;
             case 3: launch_one<MODE, CSR, true, true, 3>(L, op, smem, s); return;
-            default: launch_one<MODE, CSR, true, true, 0>(L, op, smem, s); return;
+            default: break;
         }
+        if constexpr (MODE == kPlain) {
+            switch (variant_for(MODE, CSR)) {
+                case 4: launch_one<MODE, CSR, true, true, 4>(L, op, smem, s); return;
+                case 5: launch_one<MODE, CSR, true, true, 5>(L, op, smem, s); return;
+                case 6: launch_one<MODE, CSR, true, true, 6>(L, op, smem, s); return;
+                default: break;
+            }
+        }
+        launch_one<MODE, CSR, true, true, 0>(L, op, smem, s);
+        return;
     }
     if (L.idx16) launch_one<MODE, CSR, true, false, 0>(L, op, smem, s);
     else if (L.smem) launch_one<MODE, CSR, false, true, 0>(L, op, smem, s);
@@ -374,6 +537,11 @@ void set_attr_all(size_t max_smem) {
     set_attr<MODE, CSR, true, true, 1>(max_smem);
     set_attr<MODE, CSR, true, true, 2>(max_smem);
     set_attr<MODE, CSR, true, true, 3>(max_smem);
+    if constexpr (MODE == kPlain) {
+        set_attr<MODE, CSR, true, true, 4>(max_smem);
+        set_attr<MODE, CSR, true, true, 5>(max_smem);
+        set_attr<MODE, CSR, true, true, 6>(max_smem);
+    }
     set_attr<MODE, CSR, true, false, 0>(max_smem);
     set_attr<MODE, CSR, false, true, 0>(max_smem);
     set_attr<MODE, CSR, false, false, 0>(max_smem);

@@ -98,7 +98,20 @@ bool partition_balanced(const int64_t* costs, int32_t count, int p, int32_t* bou
     return true;
 }
 
-static inline int64_t round4(int64_t x) { return (x + 3) & ~int64_t(3); }
+// Segment alignment in entries (a multiple of 4): every unit starts on a multiple of it, so with
+// 16 both the residual (4 B) and the 16-bit index streams of every unit start on a 32-byte sector.
+static int seg_align() {
+    static const int a = [] {
+        const char* e = std::getenv("PMF_SEG_ALIGN");
+        const int v = e ? std::atoi(e) : 16;
+        return v >= 4 && (v & (v - 1)) == 0 ? v : 4;
+    }();
+    return a;
+}
+static inline int64_t round_seg(int64_t x) {
+    const int64_t a = seg_align();
+    return (x + a - 1) & ~(a - 1);
+}
 
 // parallel_for over outputs [0, n_out) with chunks of equal entry counts (start = offsets)
 static void parallel_for_outputs(const int64_t* start, int32_t out_begin, int32_t n_out,
@@ -201,7 +214,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     std::vector<int64_t> seg_off(seg_len.size() + 1, 0);
     int64_t nonempty = 0;
     for (size_t s = 0; s < seg_len.size(); ++s) {
-        seg_off[s + 1] = seg_off[s] + round4(seg_len[s]);
+        seg_off[s + 1] = seg_off[s] + round_seg(seg_len[s]);
         nonempty += seg_len[s] > 0;
     }
     L.n_entries = seg_off.back();
@@ -255,7 +268,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
             const size_t s = static_cast<size_t>(p) * n_out + o;
             const int64_t real = seg_len[s];
             if (real == 0) continue;
-            const int64_t padded = round4(real);
+            const int64_t padded = round_seg(real);
             for (int64_t c = 0; c < padded; c += kUnitMax) {
                 const int64_t clen = std::min<int64_t>(kUnitMax, padded - c);
                 const int64_t creal = std::max<int64_t>(0, std::min<int64_t>(kUnitMax, real - c));

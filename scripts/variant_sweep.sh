@@ -2,7 +2,8 @@
 # Times one CCD++ outer iteration (CUDA graph) and the per-sweep split for each launch variant.
 for v in ${@:-0 1 2 3}; do
   echo "== PMF_SWEEP_VARIANT=$v"
-  PMF_SWEEP_VARIANT=$v python - <<'PY'
+  if [ "$v" = default ]; then unset PMF_SWEEP_VARIANT; else export PMF_SWEEP_VARIANT=$v; fi
+  python - <<'PY'
 import sys, os
 sys.path.insert(0, os.getcwd())
 import bench, paper_1511_02433_b200 as P
