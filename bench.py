@@ -146,6 +146,8 @@ def run_ours(args, rank, world, dist):
     t0 = time.perf_counter()
     ctx = P.Context(A, device=device, rank=rank, world=world, nccl_id=nccl_id)
     log(f"[bench] context (layouts + upload) {time.perf_counter() - t0:.1f}s")
+    for side, li in ctx.layout_info().items():
+        log(f"[bench] layout {side}: " + " ".join(f"{k}={v}" for k, v in li.items()))
     ctx.set_probe(probe)
     pk = peaks()
     hbm = pk.get("hbm_gbs", 6650.0)

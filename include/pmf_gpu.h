@@ -164,6 +164,16 @@ pmf_status pmf_ctx_launch_count(pmf_ctx* ctx, int64_t* per_iteration);
  * 1/2/4/8 the per-class sums of ceil(len / (4 * lanes * unroll)) group-steps; rest 0). */
 pmf_status pmf_ctx_debug_sweep_profile(pmf_ctx* ctx, int32_t side, int32_t promote, uint64_t* cta_ns,
                                       int64_t* cta_stats, int32_t* n_ctas);
+/* Diagnostic: the device layout of one side (0 = CSR / u-sweep, 1 = CSC / v-sweep). */
+typedef struct pmf_layout_info {
+    int32_t n_panels, panel_size;   /* gather panels staged in shared memory, and their width */
+    int32_t smem, idx16;            /* 1: panel-staged gathers / 16-bit panel-local indices */
+    int32_t promote_fused;          /* 1: promote fused into one sweep; 0: residual pass + sweep */
+    int32_t rmw_sub, sub_width;     /* residual pass sub-panels (split promote) and their width */
+    int32_t n_units, n_slots, ctas;
+    int64_t n_entries, n_real;      /* padded / real entries */
+} pmf_layout_info;
+pmf_status pmf_ctx_layout_info(pmf_ctx* ctx, int32_t side, pmf_layout_info* out);
 /* Enables (1) / disables (0) per-sweep CUDA-event timing inside pmf_ctx_ccdpp_iterate. */
 pmf_status pmf_ctx_set_profiling(pmf_ctx* ctx, int32_t on);
 

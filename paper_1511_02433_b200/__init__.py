@@ -89,6 +89,12 @@ class _Totals(C.Structure):
                 ("d2h_bytes", C.c_int64), ("kernel_launches", C.c_int64)]
 
 
+class _LayoutInfo(C.Structure):
+    _fields_ = [(f, C.c_int32) for f in ("n_panels", "panel_size", "smem", "idx16", "promote_fused", "rmw_sub",
+                                         "sub_width", "n_units", "n_slots", "ctas")] + \
+               [("n_entries", C.c_int64), ("n_real", C.c_int64)]
+
+
 _P = C.c_void_p
 _SIGS = {
     "pmf_last_error": ([], C.c_char_p),
@@ -112,6 +118,7 @@ _SIGS = {
     "pmf_ctx_get_residual": ([_P, _P, _P], C.c_int),
     "pmf_ctx_kernel_stats": ([_P, _P, _P, _P, _P], C.c_int),
     "pmf_ctx_set_profiling": ([_P, C.c_int32], C.c_int),
+    "pmf_ctx_layout_info": ([_P, C.c_int32, _P], C.c_int),
     "pmf_ctx_launch_count": ([_P, _P], C.c_int),
     "pmf_ctx_debug_sweep_profile": ([_P, C.c_int32, C.c_int32, _P, _P, _P], C.c_int),
     "pmf_ccdpp_build_rhat": ([_P, _P, _P, _P, _P], C.c_int),
@@ -671,6 +678,18 @@ class Context:
 
     def set_profiling(self, on: bool):
         _check(lib.pmf_ctx_set_profiling(self.h, 1 if on else 0))
+
+    def layout_info(self) -> dict:
+        """Device layout of both sides (panels, promote split, units) -- pmf_ctx_layout_info."""
+        out = {}
+        for side, name in ((0, "csr"), (1, "csc")):
+            li = _LayoutInfo()
+            _check(lib.pmf_ctx_layout_info(self.h, side, C.byref(li)))
+            d = {f: getattr(li, f) for f, _ in li._fields_}
+            for f in ("smem", "idx16", "promote_fused"):
+                d[f] = bool(d[f])
+            out[name] = d
+        return out
 
     def debug_sweep_profile(self, side: int, promote: bool = False):
         n = C.c_int32()

@@ -105,13 +105,48 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
         : "memory");
 }
 
+// Streaming loads of read-only data (indices always; the residual in plain sweeps): ld.global.cs.
+// -DPMF_STREAM_NOALLOC selects ld.global.nc.L1::no_allocate (measured slower: wide-panel v-sweep
+// 188 -> 208 us, Yahoo sweeps +20 %).
+__device__ __forceinline__ float4 ld_stream(const float4* p) {
+#ifndef PMF_STREAM_NOALLOC
+    return __ldcs(p);
+#else
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+#endif
+}
+__device__ __forceinline__ uint2 ld_stream(const uint2* p) {
+#ifndef PMF_STREAM_NOALLOC
+    return __ldcs(p);
+#else
+    uint2 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
+    return v;
+#endif
+}
+__device__ __forceinline__ int4 ld_stream(const int4* p) {
+#ifndef PMF_STREAM_NOALLOC
+    return __ldcs(p);
+#else
+    int4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p));
+    return v;
+#endif
+}
+
 template <bool IDX16>
 struct IdxVec;
 template <>
 struct IdxVec<true> {
     using raw_t = uint2;
     __device__ __forceinline__ static raw_t load(const void* base, int64_t e) {
-        return __ldcs(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(base) + e));
+        return ld_stream(reinterpret_cast<const uint2*>(static_cast<const uint16_t*>(base) + e));
     }
     __device__ __forceinline__ static int get(const raw_t& r, int q) {
         const uint32_t w = q < 2 ? r.x : r.y;
@@ -122,7 +157,7 @@ template <>
 struct IdxVec<false> {
     using raw_t = int4;
     __device__ __forceinline__ static raw_t load(const void* base, int64_t e) {
-        return __ldcs(reinterpret_cast<const int4*>(static_cast<const int32_t*>(base) + e));
+        return ld_stream(reinterpret_cast<const int4*>(static_cast<const int32_t*>(base) + e));
     }
     __device__ __forceinline__ static int get(const raw_t& r, int q) {
         return q == 0 ? r.x : q == 1 ? r.y : q == 2 ? r.z : r.w;
@@ -138,6 +173,10 @@ struct Roles {
 
 __host__ __device__ __forceinline__ int stage_stride(int panel_size) { return ((panel_size + 1) + 3) & ~3; }
 
+// A thief restages its shared-memory panel only for a piece with at least this much work left
+// (entries, estimated from the remaining long / medium / short units).
+constexpr int kStealRestageMin = 16384;
+
 // Processes units [ub, ue) of the current piece in warp batches of 32/G units, one unit per group
 // of G lanes.  `counter` is the piece's shared counter for this length class.
 template <int MODE, bool CSR, bool IDX16, int G, int kUnroll>
@@ -151,15 +190,21 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
     const int g = lane / G;   // group within the warp
     const int gl = lane % G;  // lane within the group
     if (ub >= ue) return;
-    int nb = 0;
-    if (lane == 0) nb = atomicAdd(counter, B);
-    nb = __shfl_sync(0xffffffffu, nb, 0);
+    // Batches are claimed two ahead: the claim for batch b+2 is issued while batch b starts and
+    // consumed (shuffle + descriptor load) one batch later, so the counter's latency (a global
+    // atomic when pieces are shared for stealing) never stalls the in-order warp.
+    int a = 0, a1 = 0;
+    if (lane == 0) a = atomicAdd(counter, B);
+    int nb = __shfl_sync(0xffffffffu, a, 0);
     Unit Un = (nb + g < ue) ? units[nb + g] : Unit{0u, 0, 0, -2};
+    if (lane == 0) a1 = atomicAdd(counter, B);
     while (nb < ue) {
         const Unit U = Un;
-        // prefetch the next batch's descriptors while this one streams
-        if (lane == 0) nb = atomicAdd(counter, B);
-        nb = __shfl_sync(0xffffffffu, nb, 0);
+        int a2 = 0;
+        if (lane == 0) a2 = atomicAdd(counter, B);
+        // descriptors of the next batch (claimed one batch ago) while this one streams
+        nb = __shfl_sync(0xffffffffu, a1, 0);
+        a1 = a2;
         Un = (nb + g < ue) ? units[nb + g] : Unit{0u, 0, 0, -2};
 
         const int32_t oidx = op.out_off + U.o;
@@ -182,8 +227,8 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
 #pragma unroll
             for (int q = 0; q < kUnroll; ++q) {
                 if (4 * G * q < rem) {
-                    r4[q] = __ldcs(rp + G * q);
-                    ix[q] = __ldcs(ip + G * q);
+                    r4[q] = MODE == kPlain ? ld_stream(rp + G * q) : __ldcs(rp + G * q);
+                    ix[q] = ld_stream(ip + G * q);
                 }
             }
 #pragma unroll
@@ -243,6 +288,86 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
     }
 }
 
+// Residual pass of a split promote over one sub-panel q of the piece's panel: the unit's entries
+// whose gather index falls in sub-panel q are [lo, hi) (usplit, ascending indices), processed as
+// 128-bit vectors from lo & ~3 with a per-entry range predicate.  A vector straddling two
+// sub-panels is rewritten in both sub-passes; they run one after the other in this CTA (the piece
+// is this CTA's), so the second sees the first's stores.  Same arithmetic as the fused promote.
+template <bool CSR, bool IDX16, int G, int kUnroll>
+__device__ __noinline__ void run_rmw_sub(int* counter, int32_t ub, int32_t ue, const Unit* __restrict__ units,
+                                         const uint16_t* __restrict__ usplit, int S, int q, int32_t gofs,
+                                         const void* __restrict__ idx, float* __restrict__ R,
+                                         const SweepOperands& op, const float* ga, const float* gb) {
+    using IV = IdxVec<IDX16>;
+    constexpr int B = 32 / G;
+    const int lane = threadIdx.x & 31;
+    const int g = lane / G;
+    const int gl = lane % G;
+    if (ub >= ue) return;
+    for (;;) {
+        int nb = 0;
+        if (lane == 0) nb = atomicAdd(counter, B);
+        nb = __shfl_sync(0xffffffffu, nb, 0);
+        if (nb >= ue) break;
+        const int32_t u = nb + g;
+        int lo = 0, hi = 0;
+        int64_t e0 = 0;
+        float oa = 0.f, ob = 0.f;
+        if (u < ue) {
+            const Unit U = units[u];
+            const uint16_t* sp = usplit + static_cast<int64_t>(u) * (S + 1) + q;
+            lo = sp[0];
+            hi = sp[1];
+            e0 = U.e0;
+            if (hi > lo) {
+                oa = __ldg(op.oa + op.out_off + U.o);
+                ob = __ldg(op.ob + op.out_off + U.o);
+            }
+        }
+        const int v0 = lo & ~3;
+        const int nvec = hi > lo ? (hi - v0 + 3) >> 2 : 0;
+        const int my_steps = (nvec + G * kUnroll - 1) / (G * kUnroll);
+        const int steps = static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(my_steps)));
+        float4* rp = reinterpret_cast<float4*>(R + e0 + v0);
+        const typename IV::raw_t* ip = reinterpret_cast<const typename IV::raw_t*>(
+            static_cast<const char*>(idx) + (e0 + v0) * (IDX16 ? 2 : 4));
+        for (int s = 0; s < steps; ++s) {
+            float4 r4[kUnroll];
+            typename IV::raw_t ix[kUnroll];
+#pragma unroll
+            for (int x = 0; x < kUnroll; ++x) {
+                const int vi = gl + G * (kUnroll * s + x);
+                if (vi < nvec) {
+                    r4[x] = __ldcs(rp + vi);
+                    ix[x] = ld_stream(ip + vi);
+                }
+            }
+#pragma unroll
+            for (int x = 0; x < kUnroll; ++x) {
+                const int vi = gl + G * (kUnroll * s + x);
+                if (vi < nvec) {
+                    float rv[4] = {r4[x].x, r4[x].y, r4[x].z, r4[x].w};
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const int pos = v0 + 4 * vi + c;
+                        if (pos >= lo && pos < hi) {
+                            const int gi = IV::get(ix[x], c) - gofs;
+                            const float a = ga[gi];
+                            const float b = gb[gi];
+                            float r = __fsub_rn(rv[c], __fmul_rn(oa, a));
+                            const float w = CSR ? ob : b;
+                            const float h = CSR ? b : ob;
+                            if (w != 0.f) r = __fadd_rn(r, __fmul_rn(w, h));
+                            rv[c] = r;
+                        }
+                    }
+                    __stcs(rp + vi, make_float4(rv[0], rv[1], rv[2], rv[3]));
+                }
+            }
+        }
+    }
+}
+
 // Plain-sweep variant of run_class with the loads software-pipelined across steps and unit
 // batches: a warp walks the flattened sequence of (batch, step) pairs and issues the loads of the
 // next pair before gathering and accumulating the current one, so its loads are in flight
@@ -268,8 +393,8 @@ __device__ __forceinline__ void pipe_load(PipeBuf<IDX16, G, kUnroll>& b, const U
 #pragma unroll
     for (int q = 0; q < kUnroll; ++q) {
         const bool in = 4 * G * q < b.rem;
-        b.r[q] = in ? __ldcs(rp + G * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        b.ix[q] = in ? __ldcs(ip + G * q) : typename IdxVec<IDX16>::raw_t{};
+        b.r[q] = in ? ld_stream(rp + G * q) : make_float4(0.f, 0.f, 0.f, 0.f);
+        b.ix[q] = in ? ld_stream(ip + G * q) : typename IdxVec<IDX16>::raw_t{};
     }
 }
 
@@ -379,7 +504,8 @@ __global__ void __launch_bounds__(Var<V>::NT, 1)
 sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
              const int32_t* __restrict__ piece_start, const int32_t* __restrict__ panel_base,
              const void* __restrict__ idx, float* __restrict__ R, float2* __restrict__ partial,
-             SweepOperands op, int32_t panel_size) {
+             SweepOperands op, int32_t panel_size, const uint16_t* __restrict__ usplit, int32_t rmw_sub,
+             int* __restrict__ gcnt, int32_t n_pieces) {
     extern __shared__ __align__(16) float smem[];
     __shared__ int s_next[3];
     __shared__ __align__(8) uint64_t s_bar;
@@ -398,45 +524,126 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
     uint32_t phase = 0;
 
     const int pb = piece_start[blockIdx.x], pe = piece_start[blockIdx.x + 1];
-    for (int pc = pb; pc < pe; ++pc) {
+    // split-promote residual pass: the panel is staged in rmw_sub sub-panels of width panel_size
+    const int nsub = MODE == kRmw ? rmw_sub : 1;
+    // Work stealing (single-pass sweeps): the unit counters of every piece live in global memory
+    // (gcnt[4 * piece + class], absolute unit indices), so a CTA that has finished its own pieces
+    // scans all pieces and joins the one with the most remaining work; the last CTA to finish
+    // resets the counters for the next launch.
+    const bool steal = gcnt != nullptr && nsub == 1;
+    __shared__ int s_victim;
+    int cur_panel = -1;
+    int own = pb;
+    for (;;) {
+        int pc;
+        if (own < pe) {
+            pc = own++;
+        } else {
+            if (!steal) break;
+            __syncthreads();  // the previous piece is fully consumed
+            if (threadIdx.x < 32) {
+                // remaining work per piece (entries, roughly: long / medium / short units)
+                int best = -1, bestw = 0;
+                for (int p = threadIdx.x; p < n_pieces; p += 32) {
+                    const Piece z = pieces[p];
+                    const volatile int* g = gcnt + 4 * p;
+                    const int r0 = max(0, z.um - g[0]), r1 = max(0, z.us - g[1]), r2 = max(0, z.ue - g[2]);
+                    int w = r0 * 512 + r1 * 96 + r2 * 32;
+                    if (z.panel != cur_panel && w < kStealRestageMin) w = 0;  // not worth a restage
+                    if (w > bestw) {
+                        bestw = w;
+                        best = p;
+                    }
+                }
+#pragma unroll
+                for (int off = 16; off > 0; off >>= 1) {
+                    const int ow = __shfl_xor_sync(0xffffffffu, bestw, off);
+                    const int ob = __shfl_xor_sync(0xffffffffu, best, off);
+                    if (ow > bestw || (ow == bestw && ob > best)) {
+                        bestw = ow;
+                        best = ob;
+                    }
+                }
+                if (threadIdx.x == 0) s_victim = best;
+            }
+            __syncthreads();
+            pc = s_victim;
+            if (pc < 0) break;
+        }
         const Piece pz = pieces[pc];
-        __syncthreads();  // previous piece fully consumed (and barrier initialised)
-        if (threadIdx.x == 0) {
-            s_next[0] = pz.ub;
-            s_next[1] = pz.um;
-            s_next[2] = pz.us;
-            if (SMEM) {
-                const int32_t gbase = panel_base[pz.panel];
-                const int len = panel_base[pz.panel + 1] - gbase;
-                const uint32_t bytes = static_cast<uint32_t>(((len + 3) & ~3) * sizeof(float));
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&s_bar, bytes * A);
-                bulk_g2s(s0, (MODE == kPlain ? op.gn : op.ga) + gbase, bytes, &s_bar);
-                if (A >= 2) bulk_g2s(s1, op.gb + gbase, bytes, &s_bar);
-                if (A >= 3) bulk_g2s(s2, op.gn + gbase, bytes, &s_bar);
+        int* c0 = steal ? gcnt + 4 * pc : &s_next[0];
+        int* c1 = steal ? gcnt + 4 * pc + 1 : &s_next[1];
+        int* c2 = steal ? gcnt + 4 * pc + 2 : &s_next[2];
+        for (int q = 0; q < nsub; ++q) {
+            const int32_t gbase = panel_base[pz.panel] + q * panel_size;
+            const int len = nsub > 1 ? min(panel_size, panel_base[pz.panel + 1] - gbase)
+                                     : panel_base[pz.panel + 1] - gbase;
+            if (nsub > 1 && len <= 0) break;  // uniform: no index of this panel lies beyond
+            const bool stage = nsub > 1 || pz.panel != cur_panel;
+            __syncthreads();  // previous piece / sub-pass fully consumed (and barrier initialised)
+            if (threadIdx.x == 0) {
+                s_next[0] = pz.ub;
+                s_next[1] = pz.um;
+                s_next[2] = pz.us;
+                if (SMEM && stage) {
+                    const uint32_t bytes = static_cast<uint32_t>(((len + 3) & ~3) * sizeof(float));
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    mbar_expect_tx(&s_bar, bytes * A);
+                    bulk_g2s(s0, (MODE == kPlain ? op.gn : op.ga) + gbase, bytes, &s_bar);
+                    if (A >= 2) bulk_g2s(s1, op.gb + gbase, bytes, &s_bar);
+                    if (A >= 3) bulk_g2s(s2, op.gn + gbase, bytes, &s_bar);
+                }
+            }
+            if (SMEM && stage) {
+                mbar_wait(&s_bar, phase);
+                phase ^= 1;
+                if (threadIdx.x == 0) {
+                    s0[panel_size] = 0.f;  // sentinel slot of padding entries
+                    if (A >= 2) s1[panel_size] = 0.f;
+                    if (A >= 3) s2[panel_size] = 0.f;
+                }
+            }
+            cur_panel = nsub > 1 ? -1 : pz.panel;
+            __syncthreads();
+            const float* g0 = SMEM ? s0 : (MODE == kPlain ? op.gn : op.ga);
+            const float* g1 = SMEM ? s1 : op.gb;
+            const float* g2 = SMEM ? s2 : op.gn;
+            if constexpr (MODE == kRmw && SMEM) {
+                if (nsub > 1) {
+                    const int32_t gofs = q * panel_size;
+                    run_rmw_sub<CSR, IDX16, 8, Var<V>::UA>(&s_next[0], pz.ub, pz.um, units, usplit, nsub, q, gofs, idx, R, op, g0, g1);
+                    run_rmw_sub<CSR, IDX16, 4, Var<V>::UB>(&s_next[1], pz.um, pz.us, units, usplit, nsub, q, gofs, idx, R, op, g0, g1);
+                    run_rmw_sub<CSR, IDX16, 2, Var<V>::UC>(&s_next[2], pz.us, pz.ue, units, usplit, nsub, q, gofs, idx, R, op, g0, g1);
+                    continue;
+                }
+            }
+            if constexpr (MODE == kPlain && kPipelined<V>) {
+                run_class_pipe<IDX16, 8, Var<V>::UA>(c0, pz.ub, pz.um, units, idx, R, partial, op, g0);
+                run_class_pipe<IDX16, 4, Var<V>::UB>(c1, pz.um, pz.us, units, idx, R, partial, op, g0);
+                run_class_pipe<IDX16, 2, Var<V>::UC>(c2, pz.us, pz.ue, units, idx, R, partial, op, g0);
+            } else {
+                run_class<MODE, CSR, IDX16, 8, Var<V>::UA>(c0, pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
+                run_class<MODE, CSR, IDX16, 4, Var<V>::UB>(c1, pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
+                run_class<MODE, CSR, IDX16, 2, Var<V>::UC>(c2, pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
             }
         }
-        if (SMEM) {
-            mbar_wait(&s_bar, phase);
-            phase ^= 1;
-            if (threadIdx.x == 0) {
-                s0[panel_size] = 0.f;  // sentinel slot of padding entries
-                if (A >= 2) s1[panel_size] = 0.f;
-                if (A >= 3) s2[panel_size] = 0.f;
-            }
+    }
+    if (steal) {
+        // the last CTA out resets every piece's counters to its class starts for the next launch
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            s_victim = atomicAdd(gcnt + 4 * n_pieces, 1) == static_cast<int>(gridDim.x) - 1;
         }
         __syncthreads();
-        const float* g0 = SMEM ? s0 : (MODE == kPlain ? op.gn : op.ga);
-        const float* g1 = SMEM ? s1 : op.gb;
-        const float* g2 = SMEM ? s2 : op.gn;
-        if constexpr (MODE == kPlain && kPipelined<V>) {
-            run_class_pipe<IDX16, 8, Var<V>::UA>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0);
-            run_class_pipe<IDX16, 4, Var<V>::UB>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0);
-            run_class_pipe<IDX16, 2, Var<V>::UC>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0);
-        } else {
-            run_class<MODE, CSR, IDX16, 8, Var<V>::UA>(&s_next[0], pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
-            run_class<MODE, CSR, IDX16, 4, Var<V>::UB>(&s_next[1], pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
-            run_class<MODE, CSR, IDX16, 2, Var<V>::UC>(&s_next[2], pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
+        if (s_victim) {
+            for (int p = threadIdx.x; p < n_pieces; p += blockDim.x) {
+                const Piece z = pieces[p];
+                gcnt[4 * p] = z.ub;
+                gcnt[4 * p + 1] = z.um;
+                gcnt[4 * p + 2] = z.us;
+            }
+            if (threadIdx.x == 0) gcnt[4 * n_pieces] = 0;
         }
     }
     if (op.cta_clock) {
@@ -449,45 +656,100 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
     }
 }
 
-// Fixed-order combination of the partial sums of outputs with several (or zero) units.
+// Fixed-order combination of the partial sums of outputs with several (or zero) units: the dense
+// slots p * n_out + o over the panels in order, then the output's overflow slots.  Outputs
+// [0, n_big) have many slots: a warp each (lane-strided, xor tree); the rest a thread each
+// (sequential, the dense slots of adjacent outputs are adjacent: coalesced).
+constexpr int kFinalizeThreads = 256;
 __global__ void finalize_kernel(const int32_t* __restrict__ mo_out, const int32_t* __restrict__ mo_start,
-                                int32_t n_mo, const float2* __restrict__ partial, float* __restrict__ out,
+                                int32_t n_mo, int32_t n_big, int32_t big_blocks, const float2* __restrict__ partial,
+                                int32_t n_panels, int32_t n_out, int64_t n_dense, float* __restrict__ out,
                                 int32_t out_off, float lambda) {
-    const int lane = threadIdx.x & 31;
-    const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-    const int64_t nw = (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5;
-    for (int64_t q = wid; q < n_mo; q += nw) {
-        const int s0 = mo_start[q], s1 = mo_start[q + 1];
-        float num = 0.f, den = 0.f;
-        for (int s = s0 + lane; s < s1; s += 32) {
-            const float2 p = partial[s];
-            num += p.x;
-            den += p.y;
-        }
+    const float2* ovf = partial + n_dense;
+    if (static_cast<int32_t>(blockIdx.x) < big_blocks) {
+        const int lane = threadIdx.x & 31;
+        const int64_t wid = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+        const int64_t nw = (static_cast<int64_t>(big_blocks) * blockDim.x) >> 5;
+        for (int64_t q = wid; q < n_big; q += nw) {
+            const int o = mo_out[q];
+            const int s0 = mo_start[q], s1 = mo_start[q + 1];
+            float num = 0.f, den = 0.f;
+            for (int p = lane; p < n_panels; p += 32) {
+                const float2 v = partial[static_cast<int64_t>(p) * n_out + o];
+                num += v.x;
+                den += v.y;
+            }
+            for (int s = s0 + lane; s < s1; s += 32) {
+                const float2 v = ovf[s];
+                num += v.x;
+                den += v.y;
+            }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
-            num += __shfl_xor_sync(0xffffffffu, num, off);
-            den += __shfl_xor_sync(0xffffffffu, den, off);
+            for (int off = 16; off > 0; off >>= 1) {
+                num += __shfl_xor_sync(0xffffffffu, num, off);
+                den += __shfl_xor_sync(0xffffffffu, den, off);
+            }
+            if (lane == 0) {
+                const float dt = __fadd_rn(lambda, den);
+                out[out_off + o] = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+            }
         }
-        if (lane == 0) {
-            const float dt = __fadd_rn(lambda, den);
-            out[out_off + mo_out[q]] = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
-        }
+        return;
     }
+    const int64_t q = n_big + static_cast<int64_t>(blockIdx.x - big_blocks) * blockDim.x + threadIdx.x;
+    if (q >= n_mo) return;
+    const int o = mo_out[q];
+    const int s0 = mo_start[q], s1 = mo_start[q + 1];
+    float num = 0.f, den = 0.f;
+#pragma unroll 4
+    for (int p = 0; p < n_panels; ++p) {
+        const float2 v = partial[static_cast<int64_t>(p) * n_out + o];
+        num += v.x;
+        den += v.y;
+    }
+    for (int s = s0; s < s1; ++s) {
+        const float2 v = ovf[s];
+        num += v.x;
+        den += v.y;
+    }
+    const float dt = __fadd_rn(lambda, den);
+    out[out_off + o] = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+}
+
+// Work stealing is on for layouts of short segments, whose per-CTA cost the static partition
+// predicts poorly (Yahoo-Music shape: max/avg CTA time 1.4 -> 1.01); on long-segment layouts the
+// static partition is already within a few % and the shared counters cost more than they recover.
+// PMF_STEAL=0 / 1 forces it off / on.
+bool steal_enabled(const DevSweep& L) {
+    static const int force = [] {
+        const char* e = std::getenv("PMF_STEAL");
+        return e ? std::atoi(e) : -1;
+    }();
+    return force >= 0 ? force != 0 : L.avg_segment < 64.0;
 }
 
 template <int MODE, bool CSR, bool IDX16, bool SMEM, int V>
 void launch_one(const DevSweep& L, const SweepOperands& op, size_t smem, cudaStream_t s) {
+    const bool sub = MODE == kRmw && L.rmw_sub > 1;
     sweep_kernel<MODE, CSR, IDX16, SMEM, V><<<L.ctas, Var<V>::NT, smem, s>>>(
-        L.units, L.pieces, L.piece_start, L.panel_base, L.idx, L.R, L.partial, op, L.panel_size);
+        L.units, L.pieces, L.piece_start, L.panel_base, L.idx, L.R, L.partial, op,
+        sub ? L.sub_width : L.panel_size, L.usplit, sub ? L.rmw_sub : 1, steal_enabled(L) ? L.gcnt : nullptr,
+        L.n_pieces);
 }
 
 int variant_for(int mode, bool csr) {
-    static const int plain = [] {
-        const char* e = std::getenv("PMF_SWEEP_VARIANT");
-        return e ? std::atoi(e) : -1;
+    // PMF_SWEEP_VARIANT (both sides) / PMF_SWEEP_VARIANT_CSR / _CSC override the plain-sweep default
+    static const int plain_csr = [] {
+        const char* e = std::getenv("PMF_SWEEP_VARIANT_CSR");
+        if (!e) e = std::getenv("PMF_SWEEP_VARIANT");
+        return e ? std::atoi(e) : kDefaultPlainVariantCsr;
     }();
-    if (mode == kPlain && plain < 0) return csr ? kDefaultPlainVariantCsr : kDefaultPlainVariantCsc;
+    static const int plain_csc = [] {
+        const char* e = std::getenv("PMF_SWEEP_VARIANT_CSC");
+        if (!e) e = std::getenv("PMF_SWEEP_VARIANT");
+        return e ? std::atoi(e) : kDefaultPlainVariantCsc;
+    }();
+    const int plain = csr ? plain_csr : plain_csc;
     static const int promote = [] {
         const char* e = std::getenv("PMF_PROMOTE_VARIANT");
         return e ? std::atoi(e) : kDefaultPromoteVariant;
@@ -552,7 +814,8 @@ void set_attr_all(size_t max_smem) {
 size_t sweep_smem_bytes(const DevSweep& L, SweepMode mode, bool csr_side) {
     if (!L.smem) return 0;
     const int arrays = mode == kPromote ? (csr_side ? 2 : 3) : mode == kRmw ? 2 : 1;
-    return static_cast<size_t>(arrays) * stage_stride(L.panel_size) * sizeof(float);
+    const int width = mode == kRmw && L.rmw_sub > 1 ? L.sub_width : L.panel_size;
+    return static_cast<size_t>(arrays) * stage_stride(width) * sizeof(float);
 }
 
 void sweep_set_attributes(size_t max_smem) {
@@ -568,6 +831,11 @@ void sweep_set_attributes(size_t max_smem) {
 
 int launch_sweep(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOperands& op,
                  cudaStream_t stream) {
+    if (mode == kPromote && L.smem && !L.promote_fused) {
+        // the promote's staged vectors do not fit beside each other at this panel width: residual
+        // pass over sub-panels, then a plain sweep (bitwise the same residual and result)
+        return launch_sweep(L, kRmw, csr_side, op, stream) + launch_sweep(L, kPlain, csr_side, op, stream);
+    }
     const size_t smem = sweep_smem_bytes(L, mode, csr_side);
     int launched = 0;
     if (L.n_units > 0) {
@@ -587,11 +855,12 @@ int launch_sweep(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOp
         ++launched;
     }
     if (mode != kDemote && mode != kRmw && L.n_mo > 0) {
-        const int threads = 256;
-        const int64_t warps = L.n_mo;
-        const int blocks = static_cast<int>(std::min<int64_t>((warps * 32 + threads - 1) / threads, 4096));
-        finalize_kernel<<<blocks, threads, 0, stream>>>(L.mo_out, L.mo_start, L.n_mo, L.partial, op.out,
-                                                        op.out_off, op.lambda);
+        const int big_blocks = static_cast<int>(std::min<int64_t>(
+            (static_cast<int64_t>(L.n_mo_big) * 32 + kFinalizeThreads - 1) / kFinalizeThreads, 1184));
+        const int small_blocks = (L.n_mo - L.n_mo_big + kFinalizeThreads - 1) / kFinalizeThreads;
+        finalize_kernel<<<big_blocks + small_blocks, kFinalizeThreads, 0, stream>>>(
+            L.mo_out, L.mo_start, L.n_mo, L.n_mo_big, big_blocks, L.partial, L.n_dense ? L.n_panels : 0, L.n_out,
+            L.n_dense, op.out, op.out_off, op.lambda);
         ++launched;
     }
     return launched;

@@ -25,6 +25,14 @@ struct DevSweep {
     int32_t* mo_out = nullptr;
     int32_t* mo_start = nullptr;
     float2* partial = nullptr;
+    int32_t n_mo_big = 0;
+    int64_t n_dense = 0;            // partial[p * n_out + o]: first chunk of segment (p, o)
+    int32_t n_pieces = 0;
+    double avg_segment = 0.0;
+    int* gcnt = nullptr;            // 4 per piece (class counters) + 1 (CTAs done): work stealing
+    bool promote_fused = true;      // else: rmw_sub residual sub-passes + a plain sweep
+    int32_t rmw_sub = 1, sub_width = 0;
+    uint16_t* usplit = nullptr;     // rmw_sub > 1: per unit rmw_sub+1 offsets
 };
 
 // kRmw: the promote's residual update alone (R <- (R - u'v') + [w != 0] w h), no accumulation

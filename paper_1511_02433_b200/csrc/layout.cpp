@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <numeric>
 #include <stdexcept>
+#include <string>
 #include <thread>
 
 namespace pmfgpu {
@@ -98,8 +99,11 @@ bool partition_balanced(const int64_t* costs, int32_t count, int p, int32_t* bou
     return true;
 }
 
-// Segment alignment in entries (a multiple of 4): every unit starts on a multiple of it, so with
-// 16 both the residual (4 B) and the 16-bit index streams of every unit start on a 32-byte sector.
+// Segment alignment in entries (a multiple of 4).  Segments of at least kLongSeg real entries start
+// (and are padded) on a multiple of PMF_SEG_ALIGN (default 16), so both the residual (4 B) and the
+// 16-bit index streams of their units start on a 32-byte sector; shorter segments are padded to 4
+// only (a 9-entry segment padded to 16 would stream 78 % padding).  The gap a long segment's
+// alignment leaves after its predecessor belongs to no unit and is never read.
 static int seg_align() {
     static const int a = [] {
         const char* e = std::getenv("PMF_SEG_ALIGN");
@@ -108,10 +112,9 @@ static int seg_align() {
     }();
     return a;
 }
-static inline int64_t round_seg(int64_t x) {
-    const int64_t a = seg_align();
-    return (x + a - 1) & ~(a - 1);
-}
+constexpr int64_t kLongSeg = 48;
+static inline int64_t seg_alignment(int64_t real) { return real >= kLongSeg ? seg_align() : 4; }
+static inline int64_t round_up(int64_t x, int64_t a) { return (x + a - 1) & ~(a - 1); }
 
 // parallel_for over outputs [0, n_out) with chunks of equal entry counts (start = offsets)
 static void parallel_for_outputs(const int64_t* start, int32_t out_begin, int32_t n_out,
@@ -152,9 +155,25 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     auto gidx = [&](int64_t e) -> int32_t { return gmap ? gmap[idx[e]] : idx[e]; };
 
     // ---- 1. gather panels ------------------------------------------------------------------
-    // panel width: a multiple of 4 floats so every panel base is 16-byte aligned for the TMA copy
-    int64_t pg_cap = (smem_budget_bytes / (4 * stage_arrays) - 4) & ~int64_t(3);
-    if (allow_idx16) pg_cap = std::min<int64_t>(pg_cap, 65532);
+    // Panel width: a multiple of 4 floats so every panel base is 16-byte aligned for the TMA copy.
+    // Preferred: panels narrow enough for the fused promote's `stage_arrays` vectors (one sweep per
+    // step reads and rewrites the residual).  When that cuts segments short (a wide gather space:
+    // Yahoo-Music), panels as wide as one vector allows, with the promote split into a residual pass
+    // + a plain sweep.  When even those segments are a few entries long, gathers from global memory.
+    static const int forced_arrays = [] {
+        const char* e = std::getenv("PMF_PANEL_ARRAYS");
+        return e ? std::max(1, std::min(3, std::atoi(e))) : 0;
+    }();
+    static const double min_avg = [] {  // wide panels pay off down to short segments
+        const char* e = std::getenv("PMF_PANEL_MIN_AVG");
+        return e ? std::atof(e) : 8.0;
+    }();
+    constexpr double kFusedMinAvg = 64.0;
+    auto width_cap = [&](int arrays) {
+        int64_t w = (smem_budget_bytes / (4 * arrays) - 4) & ~int64_t(3);
+        if (allow_idx16) w = std::min<int64_t>(w, 65532);
+        return w;
+    };
     const int64_t nnz_side = start[out_end] - start[out_begin];
     L.n_real = nnz_side;
     // panel of gather index g, tracked incrementally along an output's ascending indices
@@ -175,32 +194,47 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
             }
         });
     };
+    // panels of width pg: segment lengths into seg_len, returns the mean non-empty segment length
+    auto try_width = [&](int64_t pg, std::vector<int32_t>& seg_len) {
+        const int32_t np = static_cast<int32_t>((static_cast<int64_t>(gat_extent) + pg - 1) / pg);
+        count_segments(static_cast<int32_t>(pg), np, seg_len);
+        int64_t segs = 0;
+        for (auto x : seg_len) segs += x > 0;
+        return segs ? static_cast<double>(nnz_side) / segs : 0.0;
+    };
+    auto use_panels = [&](int64_t pg) {
+        L.smem = true;
+        L.panel_size = static_cast<int32_t>(pg);
+        L.n_panels = static_cast<int32_t>((static_cast<int64_t>(gat_extent) + pg - 1) / pg);
+        L.idx16 = allow_idx16;
+    };
     std::vector<int32_t> seg_len;
-    if (gat_extent <= pg_cap) {
+    const int64_t fused_w = width_cap(forced_arrays ? forced_arrays : stage_arrays);
+    const int64_t wide_w = width_cap(forced_arrays ? forced_arrays : 1);
+    if (gat_extent <= fused_w) {
         L.smem = true;
         L.panel_size = std::max(gat_extent, 1);
         L.n_panels = 1;
         L.idx16 = allow_idx16 && gat_extent <= 65535;
         count_segments(L.panel_size, 1, seg_len);
-    } else {
-        const int32_t pg = static_cast<int32_t>(pg_cap);
-        const int32_t np = static_cast<int32_t>((static_cast<int64_t>(gat_extent) + pg - 1) / pg);
-        count_segments(pg, np, seg_len);
-        int64_t segs = 0;
-        for (auto x : seg_len) segs += x > 0;
-        const double avg = segs ? static_cast<double>(nnz_side) / segs : 0.0;
-        if (avg >= 48.0) {
+    } else if (try_width(fused_w, seg_len) >= kFusedMinAvg || fused_w == wide_w) {
+        use_panels(fused_w);
+    } else if (gat_extent <= wide_w || try_width(wide_w, seg_len) >= min_avg) {
+        if (gat_extent <= wide_w) {
             L.smem = true;
-            L.panel_size = pg;
-            L.n_panels = np;
-            L.idx16 = allow_idx16;
-        } else {  // segments too short for panels: gather from global memory, 32-bit indices
-            L.smem = false;
-            L.panel_size = gat_extent;
+            L.panel_size = std::max(gat_extent, 1);
             L.n_panels = 1;
-            L.idx16 = false;
-            count_segments(std::max(gat_extent, 1), 1, seg_len);
+            L.idx16 = allow_idx16 && gat_extent <= 65535;
+            count_segments(L.panel_size, 1, seg_len);
+        } else {
+            use_panels(wide_w);
         }
+    } else {  // segments too short for panels: gather from global memory, 32-bit indices
+        L.smem = false;
+        L.panel_size = gat_extent;
+        L.n_panels = 1;
+        L.idx16 = false;
+        count_segments(std::max(gat_extent, 1), 1, seg_len);
     }
     L.sentinel = L.smem ? L.panel_size : gat_extent;
     L.panel_base.resize(L.n_panels + 1);
@@ -209,13 +243,35 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     L.panel_base[L.n_panels] = gat_extent;
     const int32_t pg = L.panel_size;
     const int32_t np = L.n_panels;
+    // promote: fused if its vectors fit next to each other, else rmw_sub sub-panel residual passes
+    if (L.smem) {
+        L.promote_fused = stage_arrays * stage_stride_floats(pg) * 4 <= smem_budget_bytes;
+        if (!L.promote_fused) {
+            int32_t S = 1;
+            for (;; ++S) {
+                const int64_t w = round_up((pg + S - 1) / S, 4);
+                if (2 * stage_stride_floats(w) * 4 <= smem_budget_bytes + 1024) break;  // + launch slack
+            }
+            L.rmw_sub = S;
+            L.sub_width = static_cast<int32_t>(round_up((pg + S - 1) / S, 4));
+        }
+    }
 
     // ---- 2. segment offsets (panel-major) ----------------------------------------------------
-    std::vector<int64_t> seg_off(seg_len.size() + 1, 0);
+    std::vector<int64_t> seg_off(seg_len.size() + 1, 0);  // start of segment s; seg_off[S] = end
+    std::vector<int64_t> seg_end(seg_len.size(), 0);
     int64_t nonempty = 0;
-    for (size_t s = 0; s < seg_len.size(); ++s) {
-        seg_off[s + 1] = seg_off[s] + round_seg(seg_len[s]);
-        nonempty += seg_len[s] > 0;
+    {
+        int64_t cur = 0;
+        for (size_t s = 0; s < seg_len.size(); ++s) {
+            const int64_t real = seg_len[s];
+            const int64_t a = real > 0 ? seg_alignment(real) : 1;
+            seg_off[s] = round_up(cur, a);
+            seg_end[s] = seg_off[s] + round_up(real, a);
+            cur = seg_end[s];
+            nonempty += real > 0;
+        }
+        seg_off[seg_len.size()] = cur;
     }
     L.n_entries = seg_off.back();
     L.avg_segment = nonempty ? static_cast<double>(nnz_side) / nonempty : 0.0;
@@ -225,14 +281,18 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     if (L.idx16) L.idx16v.alloc(L.n_entries);
     else L.idx32v.alloc(L.n_entries);
     L.val.alloc(L.n_entries);
+    auto pad = [&](int64_t w, int64_t end) {
+        for (; w < end; ++w) {
+            if (L.idx16) L.idx16v[w] = static_cast<uint16_t>(L.sentinel);
+            else L.idx32v[w] = L.sentinel;
+            L.val[w] = 0.0f;
+        }
+    };
+    // alignment gaps between segments
+    parallel_for(static_cast<int64_t>(seg_len.size()), [&](int64_t b, int64_t e) {
+        for (int64_t s = b; s < e; ++s) pad(s == 0 ? 0 : seg_end[s - 1], seg_off[s]);
+    });
     parallel_for_outputs(start, out_begin, n_out, [&](int64_t ob, int64_t oe) {
-        auto pad = [&](int64_t w, int64_t end) {
-            for (; w < end; ++w) {
-                if (L.idx16) L.idx16v[w] = static_cast<uint16_t>(L.sentinel);
-                else L.idx32v[w] = L.sentinel;
-                L.val[w] = 0.0f;
-            }
-        };
         for (int64_t o = ob; o < oe; ++o) {
             int32_t cur_p = -1;
             int64_t w = 0, wend = 0;
@@ -249,7 +309,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
                     cur_p = p;
                     const size_t sidx = static_cast<size_t>(p) * n_out + o;
                     w = seg_off[sidx];
-                    wend = seg_off[sidx + 1];
+                    wend = seg_end[sidx];
                 }
                 const int32_t local = g - L.panel_base[p];
                 if (L.idx16) L.idx16v[w] = static_cast<uint16_t>(local);
@@ -262,13 +322,14 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     });
 
     // ---- 4. units ----------------------------------------------------------------------------
-    std::vector<int32_t> cnt(n_out, 0);
+    std::vector<int32_t> cnt(n_out, 0), ovf(n_out, 0);
+    std::vector<uint8_t> chunk0;  // unit is the first chunk of its segment
     for (int32_t p = 0; p < np; ++p)
         for (int32_t o = 0; o < n_out; ++o) {
             const size_t s = static_cast<size_t>(p) * n_out + o;
             const int64_t real = seg_len[s];
             if (real == 0) continue;
-            const int64_t padded = round_seg(real);
+            const int64_t padded = seg_end[s] - seg_off[s];
             for (int64_t c = 0; c < padded; c += kUnitMax) {
                 const int64_t clen = std::min<int64_t>(kUnitMax, padded - c);
                 const int64_t creal = std::max<int64_t>(0, std::min<int64_t>(kUnitMax, real - c));
@@ -276,22 +337,41 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
                                        static_cast<int32_t>(clen), o, -1});
                 L.unit_panel.push_back(p);
                 L.unit_real.push_back(static_cast<int32_t>(creal));
+                chunk0.push_back(c == 0);
                 cnt[o]++;
+                if (c > 0) ovf[o]++;
             }
         }
-    std::vector<int32_t> slot_base(n_out, -1);
+    // Partial slots of outputs with several units (or none).  The first chunk of segment (p, o)
+    // writes the dense slot p * n_out + o: the units of a warp batch are adjacent outputs of one
+    // panel, so their 8-byte partials land in the same sectors (scattered 8-byte stores cost a
+    // 32-byte ECC read-modify-write each), and the finalize reads slot p of adjacent outputs
+    // coalesced.  Slots of (p, o) without a segment stay 0 (zeroed once).  Further chunks of a
+    // long segment go to an overflow region after the dense one, contiguous per output.
+    // Finalize order: outputs with many slots first (a warp each), then the rest (a thread each).
+    bool any_mo = false;
+    for (int32_t o = 0; o < n_out && !any_mo; ++o) any_mo = cnt[o] != 1;
+    L.n_dense = any_mo ? static_cast<int64_t>(np) * n_out : 0;
+    std::vector<int32_t> ovf_base(n_out, -1);
     L.mo_start.push_back(0);
-    for (int32_t o = 0; o < n_out; ++o) {
-        if (cnt[o] == 1) continue;
-        slot_base[o] = L.mo_start.back();
-        L.mo_out.push_back(o);
-        L.mo_start.push_back(L.mo_start.back() + cnt[o]);
-    }
-    L.n_slots = L.mo_start.back();
+    for (int pass = 0; pass < 2; ++pass)
+        for (int32_t o = 0; o < n_out; ++o) {
+            if (cnt[o] == 1 || (cnt[o] > kFinalizeWarpSlots) != (pass == 0)) continue;
+            ovf_base[o] = L.mo_start.back();
+            L.mo_out.push_back(o);
+            L.mo_start.push_back(L.mo_start.back() + ovf[o]);
+            if (pass == 0) L.n_mo_big++;
+        }
+    if (L.n_dense + L.mo_start.back() >= (int64_t(1) << 31)) throw std::length_error("too many partial slots");
+    L.n_slots = static_cast<int32_t>(L.n_dense + L.mo_start.back());
     {
         std::vector<int32_t> run(n_out, 0);
-        for (auto& u : L.units)
-            if (slot_base[u.o] >= 0) u.slot = slot_base[u.o] + run[u.o]++;
+        for (size_t x = 0; x < L.units.size(); ++x) {
+            Unit& u = L.units[x];
+            if (ovf_base[u.o] < 0) continue;
+            u.slot = chunk0[x] ? static_cast<int32_t>(static_cast<int64_t>(L.unit_panel[x]) * n_out + u.o)
+                               : static_cast<int32_t>(L.n_dense + ovf_base[u.o] + run[u.o]++);
+        }
     }
 
     // ---- 5. per-CTA pieces: contiguous unit ranges of equal cost, split at panel changes -----
@@ -315,12 +395,25 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
         for (int64_t u = ub; u < ue;) {
             int64_t v = u;
             while (v < ue && L.unit_panel[v] == L.unit_panel[u]) ++v;
-            // longest units first inside a piece: the 32/G units a warp takes together then have
-            // similar lengths (converged groups) and the long ones start early (LPT balance)
+            // Long units: longest first inside a piece (the 32/G units a warp takes together then have
+            // similar lengths, and the long ones start early: LPT balance).  Medium and short units
+            // keep their memory order inside their class, so the units of a warp batch are adjacent
+            // and its loads cover one contiguous stretch (length-sorted short units scatter a batch
+            // over the whole piece: sector-sized reads with no DRAM locality).  PMF_UNIT_ORDER=len
+            // sorts every class by length.
+            static const bool sort_all = [] {
+                const char* e = std::getenv("PMF_UNIT_ORDER");
+                return e && std::string(e) == "len";
+            }();
+            auto cls = [](int32_t len) { return len > kMidLen ? 0 : len > kShortLen ? 1 : 2; };
             std::vector<int64_t> ord(v - u);
             std::iota(ord.begin(), ord.end(), u);
-            std::stable_sort(ord.begin(), ord.end(),
-                             [&](int64_t a, int64_t b) { return L.units[a].len > L.units[b].len; });
+            std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
+                const int32_t la = L.units[a].len, lb = L.units[b].len;
+                const int ca = cls(la), cb = cls(lb);
+                if (ca != cb) return ca < cb;
+                return (sort_all || ca == 0) ? la > lb : false;
+            });
             std::vector<Unit> tu(v - u);
             std::vector<int32_t> tr(v - u);
             for (int64_t x = 0; x < v - u; ++x) {
@@ -339,6 +432,26 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
         }
         L.piece_start[c + 1] = static_cast<int32_t>(L.pieces.size());
         ub = ue;
+    }
+
+    // ---- 6. sub-panel split points of the residual pass (entries are ascending within a unit) ---
+    if (L.rmw_sub > 1) {
+        const int S = L.rmw_sub;
+        L.usplit.assign(static_cast<size_t>(nu) * (S + 1), 0);
+        parallel_for(nu, [&](int64_t b, int64_t e) {
+            for (int64_t u = b; u < e; ++u) {
+                const int64_t e0 = L.units[u].e0;
+                const int32_t real = L.unit_real[u];
+                uint16_t* sp = &L.usplit[static_cast<size_t>(u) * (S + 1)];
+                int32_t x = 0;
+                for (int q = 1; q < S; ++q) {
+                    const int64_t bound = static_cast<int64_t>(q) * L.sub_width;
+                    while (x < real && (L.idx16 ? L.idx16v[e0 + x] : L.idx32v[e0 + x]) < bound) ++x;
+                    sp[q] = static_cast<uint16_t>(x);
+                }
+                sp[S] = static_cast<uint16_t>(real);
+            }
+        });
     }
     return L;
 }

@@ -73,6 +73,7 @@ struct Unit {
 // (4-lane groups), [us, ue) short (<= kShortLen, 2-lane groups), so short segments get more units
 // in flight per warp.
 constexpr int kMidLen = 128;
+constexpr int kFinalizeWarpSlots = 32;  // outputs with more partial slots are finalized by a warp
 constexpr int kShortLen = 64;
 struct Piece {
     int32_t panel;
@@ -100,16 +101,30 @@ struct SweepLayout {
     std::vector<Piece> pieces;
     std::vector<int32_t> piece_start; // ctas + 1
     std::vector<int32_t> mo_out;      // outputs whose unit count != 1 (incl. empty outputs)
-    std::vector<int32_t> mo_start;    // size mo_out.size()+1, slot ranges
+    std::vector<int32_t> mo_start;    // size mo_out.size()+1, overflow slot ranges (after n_dense)
+    int64_t n_dense = 0;              // dense partial slots n_panels * n_out (0: no partials)
+    int32_t n_mo_big = 0;             // mo_out[0, n_mo_big): > kFinalizeWarpSlots slots
     int32_t n_slots = 0;
     int32_t ctas = 0;
     double avg_segment = 0.0;
+    // Promote (first sweep of a rank-one step): fused into one sweep when its 2 (CSR) / 3 (CSC)
+    // staged vectors fit shared memory at this panel width; otherwise a residual pass over
+    // rmw_sub sub-panels of width sub_width (2 staged vectors each) followed by a plain sweep.
+    bool promote_fused = true;
+    int32_t rmw_sub = 1;
+    int32_t sub_width = 0;
+    std::vector<uint16_t> usplit;     // rmw_sub > 1: per unit rmw_sub+1 entry offsets (0 .. real)
 };
+
+// Shared-memory floats one staged vector of `width` occupies (sentinel slot, 16-byte rounded).
+inline int64_t stage_stride_floats(int64_t width) { return ((width + 1) + 3) & ~int64_t(3); }
 
 // Builds one side.  start/idx/val: the reference's CSR (or CSC) arrays restricted to outputs
 // [out_begin, out_end) (global offsets into idx/val).  gmap maps a global gather index to the
 // padded gather space (nullptr = identity); gat_extent is that space's size.  stage_arrays is the
-// number of gather vectors the promote sweep stages (2 on the CSR side, 3 on the CSC side).
+// number of gather vectors the fused promote sweep stages (2 on the CSR side, 3 on the CSC side);
+// panels are as wide as ONE staged vector allows (the 14 plain sweeps of a step stage one), and the
+// promote is split when its vectors do not fit (PMF_PANEL_ARRAYS=n sizes panels for n vectors).
 SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const float* val,
                                int32_t out_begin, int32_t out_end, const int32_t* gmap,
                                int32_t gat_extent, int stage_arrays, int smem_budget_bytes,

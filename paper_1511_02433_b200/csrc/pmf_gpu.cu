@@ -69,7 +69,21 @@ pmf_status guard(F&& f) {
 
 [[noreturn]] void invalid(const std::string& m) { throw PmfError(PMF_INVALID_ARGUMENT, m); }
 
-constexpr int kSmemBudget = 220 * 1024;
+// Shared memory a sweep may stage per CTA.  Shared memory and L1 share 256 KB per SM and the
+// carve-out is picked from the CTA's request: up to the 196 KB configuration the streaming loads keep
+// ~60 KB of L1 and reach 7.1 TB/s next to random panel gathers; the 228 KB configuration leaves
+// ~28 KB and drops to 5.6 TB/s (scripts/micro/lds_gather.cu).  Only sweeps that stage one panel
+// this wide pay it (the fused promote; Yahoo-width plain panels, where longer segments win).
+// PMF_SMEM_BUDGET_KB overrides.
+constexpr int kSmemMax = 220 * 1024;
+int smem_budget() {
+    static const int b = [] {
+        const char* e = std::getenv("PMF_SMEM_BUDGET_KB");
+        const int kb = e ? std::atoi(e) : 220;
+        return std::max(16, std::min(kb, kSmemMax / 1024)) * 1024;
+    }();
+    return b;
+}
 
 // ---- device memory -----------------------------------------------------------------------------
 struct DevMem {
@@ -202,6 +216,9 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     D.n_entries = L.n_entries;
     D.n_units = static_cast<int32_t>(L.units.size());
     D.n_mo = static_cast<int32_t>(L.mo_out.size());
+    D.n_mo_big = L.n_mo_big;
+    D.n_dense = L.n_dense;
+    D.avg_segment = L.avg_segment;
     D.ctas = L.ctas;
     D.n_slots = L.n_slots;
     if (L.idx16) D.idx = c.mem.upload(L.idx16v, c.stream, &c.h2d);
@@ -213,11 +230,25 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     D.units = c.mem.upload(L.units, c.stream, &c.h2d);
     D.unit_panel = c.mem.upload(L.unit_panel, c.stream, &c.h2d);
     D.pieces = c.mem.upload(L.pieces, c.stream, &c.h2d);
+    D.n_pieces = static_cast<int32_t>(L.pieces.size());
+    {
+        std::vector<int32_t> g(4 * L.pieces.size() + 1, 0);
+        for (size_t p = 0; p < L.pieces.size(); ++p) {
+            g[4 * p] = L.pieces[p].ub;
+            g[4 * p + 1] = L.pieces[p].um;
+            g[4 * p + 2] = L.pieces[p].us;
+        }
+        D.gcnt = c.mem.upload(g, c.stream, &c.h2d);
+    }
     D.piece_start = c.mem.upload(L.piece_start, c.stream, &c.h2d);
     D.panel_base = c.mem.upload(L.panel_base, c.stream, &c.h2d);
     D.mo_out = c.mem.upload(L.mo_out, c.stream, &c.h2d);
     D.mo_start = c.mem.upload(L.mo_start, c.stream, &c.h2d);
     D.partial = c.mem.alloc<float2>(std::max(1, L.n_slots));
+    D.promote_fused = L.promote_fused;
+    D.rmw_sub = L.rmw_sub;
+    D.sub_width = L.sub_width;
+    if (!L.usplit.empty()) D.usplit = c.mem.upload(L.usplit, c.stream, &c.h2d);
     CUDA_TRY(cudaStreamSynchronize(c.stream));
     // keep only the metadata needed for residual readback
     L.idx16v.reset();
@@ -289,16 +320,16 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     const int32_t* cmap = c->cmap.empty() ? nullptr : c->cmap.data();
     const double t_layout = now_s();
     c->hcsr = build_sweep_layout(a->row_start, a->col_of, a->val_row, c->row_begin, c->row_end, cmap, c->ext_n,
-                                 2, kSmemBudget, c->sm_count);
+                                 2, smem_budget(), c->sm_count);
     c->hcsc = build_sweep_layout(a->col_start, a->row_of, a->val_col, c->col_begin, c->col_end, rmap, c->ext_m,
-                                 3, kSmemBudget, c->sm_count);
+                                 3, smem_budget(), c->sm_count);
     c->local_nnz_csr = a->row_start[c->row_end] - a->row_start[c->row_begin];
     c->local_nnz_csc = a->col_start[c->col_end] - a->col_start[c->col_begin];
     c->row_start_local.assign(a->row_start + c->row_begin, a->row_start + c->row_end + 1);
     c->col_start_local.assign(a->col_start + c->col_begin, a->col_start + c->col_end + 1);
     static bool attrs_set = false;
     if (!attrs_set) {
-        sweep_set_attributes(kSmemBudget + 1024);
+        sweep_set_attributes(kSmemMax + 1024);
         als_set_attributes();
         attrs_set = true;
     }
@@ -954,6 +985,27 @@ pmf_status pmf_ctx_kernel_stats(pmf_ctx* ctx, double* u_ms, int64_t* u_n, double
         if (u_n) *u_n = c.stat_u_n;
         if (v_ms) *v_ms = c.stat_v_ms;
         if (v_n) *v_n = c.stat_v_n;
+    });
+}
+
+pmf_status pmf_ctx_layout_info(pmf_ctx* ctx, int32_t side, pmf_layout_info* out) {
+    return guard([&] {
+        Ctx& c = *as_ctx(ctx);
+        if (!out) invalid("out is null");
+        if (side != 0 && side != 1) invalid("side must be 0 (CSR) or 1 (CSC)");
+        const SweepLayout& H = side == 0 ? c.hcsr : c.hcsc;
+        out->n_panels = H.n_panels;
+        out->panel_size = H.panel_size;
+        out->smem = H.smem ? 1 : 0;
+        out->idx16 = H.idx16 ? 1 : 0;
+        out->promote_fused = H.promote_fused ? 1 : 0;
+        out->rmw_sub = H.rmw_sub;
+        out->sub_width = H.sub_width;
+        out->n_units = static_cast<int32_t>(H.units.size());
+        out->n_slots = H.n_slots;
+        out->ctas = H.ctas;
+        out->n_entries = H.n_entries;
+        out->n_real = H.n_real;
     });
 }
 

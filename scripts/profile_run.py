@@ -23,8 +23,13 @@ def main():
     ap.add_argument("--iters", type=int, default=1)
     ap.add_argument("--als", type=int, default=0)
     ap.add_argument("--profiling", action="store_true", help="per-sweep event timing (no graph)")
+    ap.add_argument("--k", type=int, default=0, help="override the config's rank (fewer launches)")
+    ap.add_argument("--cta", action="store_true", help="per-CTA timing of one plain / promote sweep per side")
     a = ap.parse_args()
+    if a.cta:
+        return cta_profile(a.config)
     m, n, ntr, npr, k, lam, inner, solver = bench.CONFIGS[a.config]
+    k = a.k or k
     train, probe, A = bench.make_data(a.config)
     ctx = P.Context(A)
     if a.iters:
@@ -43,12 +48,15 @@ def main():
 
 
 
-def cta_profile():
-    """python scripts/profile_run.py --cta: per-CTA time spread of one plain u- and v-sweep."""
+def cta_profile(config):
+    """python scripts/profile_run.py --cta [--config C]: per-CTA time spread of one plain / promote
+    sweep per side (after one outer iteration at rank 4)."""
     import numpy as np
-    train, probe, A = bench.make_data("netflix-ccdpp")
+    train, probe, A = bench.make_data(config)
     ctx = P.Context(A)
-    ctx.ccdpp_begin(P.CcdConfig(k=40, lam=0.05, outer_iters=1, inner_iters=15, seed=1))
+    for side, li in ctx.layout_info().items():
+        print(f"layout {side}: " + " ".join(f"{k}={v}" for k, v in li.items()))
+    ctx.ccdpp_begin(P.CcdConfig(k=4, lam=0.05, outer_iters=1, inner_iters=15, seed=1))
     ctx.ccdpp_iterate(1)
     for side in (0, 1):
         for promote in (False, True):
@@ -65,7 +73,4 @@ def cta_profile():
 
 
 if __name__ == "__main__":
-    if "--cta" in sys.argv:
-        cta_profile()
-    else:
-        main()
+    main()

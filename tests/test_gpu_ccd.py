@@ -231,3 +231,33 @@ def test_global_gather_layout_vs_oracle(pmf, oracle):
     for r, g in zip(rep.rows, rows):
         assert rel(r.objective, g["objective"]) < 1e-4
     assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+
+
+@pytest.mark.slow
+def test_split_promote_wide_panels_residual(pmf, oracle):
+    """Both gather spaces wider than one shared-memory panel (> 56K): the 14 plain sweeps of a step
+    stage one vector per panel, and the promote (2 / 3 staged vectors, ccd.hpp:133-151 + :209-214)
+    runs as a residual pass over 2 sub-panels + a plain sweep.  Trajectory vs the oracle, residual
+    layouts bitwise equal (testutil.hpp:266-272) and true to the factors."""
+    m, n = 62000, 60000
+    t = oracle.random_triplets(m, n, 2_500_000, 13)
+    A = pmf.RatingsMatrix.from_triplets(t, m, n)
+    O = oracle.from_triplets(t, m, n)
+    ctx = pmf.Context(A)
+    lay = ctx.layout_info()
+    for side in ("csr", "csc"):
+        assert lay[side]["n_panels"] == 2 and not lay[side]["promote_fused"] and lay[side]["rmw_sub"] == 2
+    k, outer, inner = 3, 2, 3
+    ctx.ccdpp_begin(pmf.CcdConfig(k=k, lam=0.05, outer_iters=outer, inner_iters=inner, seed=4))
+    W, H, rows, _, _ = oracle.ccdpp_train(O, k, 0.05, outer, inner, 4)
+    for it in range(outer):
+        ctx.ccdpp_iterate(1)
+        assert rel(ctx.metrics()[0], rows[it]["objective"]) < 1e-4
+    model = ctx.model()
+    assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+    rr, rc = ctx.residual()
+    assert np.array_equal(rc[O.xlink], rr)
+    ri = np.repeat(np.arange(m), np.diff(O.row_start))
+    pred = np.einsum("ik,ik->i", model.w[ri].astype(np.float64), model.h[O.col_of].astype(np.float64))
+    assert np.max(np.abs(rr - (O.val_row - pred))) < 1e-4
+    ctx.close()
