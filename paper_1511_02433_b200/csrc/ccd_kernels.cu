@@ -67,8 +67,17 @@ template <>
 struct Var<6> {
     static constexpr int NT = 512, UA = 4, UB = 4, UC = 2;
 };
+// Short-segment layouts (Yahoo-Music): more independent loads in flight for the short classes.
+template <>
+struct Var<7> {
+    static constexpr int NT = 1024, UA = 4, UB = 4, UC = 4;
+};
+template <>
+struct Var<8> {
+    static constexpr int NT = 1024, UA = 2, UB = 4, UC = 4;
+};
 template <int V>
-constexpr bool kPipelined = V >= 4;
+constexpr bool kPipelined = V >= 4 && V <= 6;
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -776,6 +785,8 @@ void dispatch_idx(const DevSweep& L, const SweepOperands& op, size_t smem, cudaS
                 case 4: launch_one<MODE, CSR, true, true, 4>(L, op, smem, s); return;
                 case 5: launch_one<MODE, CSR, true, true, 5>(L, op, smem, s); return;
                 case 6: launch_one<MODE, CSR, true, true, 6>(L, op, smem, s); return;
+                case 7: launch_one<MODE, CSR, true, true, 7>(L, op, smem, s); return;
+                case 8: launch_one<MODE, CSR, true, true, 8>(L, op, smem, s); return;
                 default: break;
             }
         }
@@ -803,6 +814,8 @@ void set_attr_all(size_t max_smem) {
         set_attr<MODE, CSR, true, true, 4>(max_smem);
         set_attr<MODE, CSR, true, true, 5>(max_smem);
         set_attr<MODE, CSR, true, true, 6>(max_smem);
+        set_attr<MODE, CSR, true, true, 7>(max_smem);
+        set_attr<MODE, CSR, true, true, 8>(max_smem);
     }
     set_attr<MODE, CSR, true, false, 0>(max_smem);
     set_attr<MODE, CSR, false, true, 0>(max_smem);
@@ -829,8 +842,20 @@ void sweep_set_attributes(size_t max_smem) {
     set_attr_all<kRmw, false>(max_smem);
 }
 
+int launch_finalize(const DevSweep& L, const SweepOperands& op, cudaStream_t stream) {
+    if (L.n_mo <= 0) return 0;
+    const int big_blocks = static_cast<int>(std::min<int64_t>(
+        (static_cast<int64_t>(L.n_mo_big) * 32 + kFinalizeThreads - 1) / kFinalizeThreads, 1184));
+    const int small_blocks = (L.n_mo - L.n_mo_big + kFinalizeThreads - 1) / kFinalizeThreads;
+    finalize_kernel<<<big_blocks + small_blocks, kFinalizeThreads, 0, stream>>>(
+        L.mo_out, L.mo_start, L.n_mo, L.n_mo_big, big_blocks, L.partial, L.n_dense ? L.n_panels : 0, L.n_out,
+        L.n_dense, op.out, op.out_off, op.lambda);
+    return 1;
+}
+
 int launch_sweep(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOperands& op,
                  cudaStream_t stream) {
+    if (L.flat) return launch_flat(L, mode, csr_side, op, stream);
     if (mode == kPromote && L.smem && !L.promote_fused) {
         // the promote's staged vectors do not fit beside each other at this panel width: residual
         // pass over sub-panels, then a plain sweep (bitwise the same residual and result)
@@ -854,15 +879,7 @@ int launch_sweep(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOp
         }
         ++launched;
     }
-    if (mode != kDemote && mode != kRmw && L.n_mo > 0) {
-        const int big_blocks = static_cast<int>(std::min<int64_t>(
-            (static_cast<int64_t>(L.n_mo_big) * 32 + kFinalizeThreads - 1) / kFinalizeThreads, 1184));
-        const int small_blocks = (L.n_mo - L.n_mo_big + kFinalizeThreads - 1) / kFinalizeThreads;
-        finalize_kernel<<<big_blocks + small_blocks, kFinalizeThreads, 0, stream>>>(
-            L.mo_out, L.mo_start, L.n_mo, L.n_mo_big, big_blocks, L.partial, L.n_dense ? L.n_panels : 0, L.n_out,
-            L.n_dense, op.out, op.out_off, op.lambda);
-        ++launched;
-    }
+    if (mode != kDemote && mode != kRmw) launched += launch_finalize(L, op, stream);
     return launched;
 }
 

@@ -29,7 +29,10 @@ struct DevSweep {
     int64_t n_dense = 0;            // partial[p * n_out + o]: first chunk of segment (p, o)
     int32_t n_pieces = 0;
     double avg_segment = 0.0;
-    int* gcnt = nullptr;            // 4 per piece (class counters) + 1 (CTAs done): work stealing
+    int* gcnt = nullptr;            // 4 per piece (class / chunk counters) + 1 (CTAs done): work stealing
+    bool flat = false;              // segmented-stream layout (flat_kernels.cu)
+    FlatChunk* chunks = nullptr;
+    uint32_t* tailbits = nullptr;
     bool promote_fused = true;      // else: rmw_sub residual sub-passes + a plain sweep
     int32_t rmw_sub = 1, sub_width = 0;
     uint16_t* usplit = nullptr;     // rmw_sub > 1: per unit rmw_sub+1 offsets
@@ -60,6 +63,11 @@ struct SweepOperands {
 int launch_sweep(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOperands& op,
                  cudaStream_t stream);
 size_t sweep_smem_bytes(const DevSweep& L, SweepMode mode, bool csr_side);
+// Fixed-order finalize of outputs with partial slots (after a sweep).  Returns kernels launched.
+int launch_finalize(const DevSweep& L, const SweepOperands& op, cudaStream_t stream);
+// Flat layouts: the same contract as launch_sweep, with the segmented-stream kernels.
+int launch_flat(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOperands& op, cudaStream_t stream);
+void flat_set_attributes(size_t max_smem);
 void sweep_set_attributes(size_t max_smem);
 
 // ---- evaluation (model.hpp:103-167) -----------------------------------------------------------

@@ -256,6 +256,12 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
             L.sub_width = static_cast<int32_t>(round_up((pg + S - 1) / S, 4));
         }
     }
+    // wide panels (split promote) have short segments: segmented-stream sweeps (PMF_FLAT=0: off)
+    static const int flat_env = [] {
+        const char* e = std::getenv("PMF_FLAT");
+        return e ? std::atoi(e) : -1;
+    }();
+    L.flat = L.smem && L.idx16 && (flat_env >= 0 ? flat_env != 0 : !L.promote_fused);
 
     // ---- 2. segment offsets (panel-major) ----------------------------------------------------
     std::vector<int64_t> seg_off(seg_len.size() + 1, 0);  // start of segment s; seg_off[S] = end
@@ -265,7 +271,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
         int64_t cur = 0;
         for (size_t s = 0; s < seg_len.size(); ++s) {
             const int64_t real = seg_len[s];
-            const int64_t a = real > 0 ? seg_alignment(real) : 1;
+            const int64_t a = real > 0 ? (L.flat ? 4 : seg_alignment(real)) : 1;
             seg_off[s] = round_up(cur, a);
             seg_end[s] = seg_off[s] + round_up(real, a);
             cur = seg_end[s];
@@ -381,6 +387,11 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     for (int64_t u = 0; u < nu; ++u) {
         const int64_t len = L.units[u].len;
         const int c = len > kMidLen ? 0 : len > kShortLen ? 1 : 2;
+        if (L.flat) {  // flat sweeps: per-CTA time ~ 0.82 ns per vector + 1.45 ns per unit (fitted,
+                       // scripts/flat_fit.py, Yahoo-Music shape, both sides)
+            pre[u + 1] = pre[u] + len / 4 * 820 + 1450;
+            continue;
+        }
         pre[u + 1] = pre[u] + (len + cm.step_a[c] - 1) / cm.step_a[c] * cm.per_step_a[c] +
                      (len + cm.step_b[c] - 1) / cm.step_b[c] * cm.per_step_b[c] + len * cm.per_entry[c] +
                      cm.per_unit[c] + (u > 0 && L.unit_panel[u] != L.unit_panel[u - 1] ? cm.per_piece : 0);
@@ -411,6 +422,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
             std::stable_sort(ord.begin(), ord.end(), [&](int64_t a, int64_t b) {
                 const int32_t la = L.units[a].len, lb = L.units[b].len;
                 const int ca = cls(la), cb = cls(lb);
+                if (L.flat) return false;  // flat layouts stream units in memory order
                 if (ca != cb) return ca < cb;
                 return (sort_all || ca == 0) ? la > lb : false;
             });
@@ -423,15 +435,44 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
             std::copy(tu.begin(), tu.end(), L.units.begin() + u);
             std::copy(tr.begin(), tr.end(), L.unit_real.begin() + u);
             int64_t um = u, us = u;
-            while (um < v && L.units[um].len > kMidLen) ++um;
-            us = um;
-            while (us < v && L.units[us].len > kShortLen) ++us;
-            L.pieces.push_back(Piece{L.unit_panel[u], static_cast<int32_t>(u), static_cast<int32_t>(um),
-                                     static_cast<int32_t>(us), static_cast<int32_t>(v), {0, 0, 0}});
+            if (!L.flat) {
+                while (um < v && L.units[um].len > kMidLen) ++um;
+                us = um;
+                while (us < v && L.units[us].len > kShortLen) ++us;
+            }
+            Piece pz{L.unit_panel[u], static_cast<int32_t>(u), static_cast<int32_t>(um),
+                     static_cast<int32_t>(us), static_cast<int32_t>(v), {0, 0, 0}};
+            if (L.flat) {  // chunks of whole units: <= kFlatChunkVectors vectors (one unit if longer), <= kFlatChunkUnits units
+                pz.pad[0] = static_cast<int32_t>(L.chunks.size());
+                for (int64_t x = u; x < v;) {
+                    const int32_t v0 = static_cast<int32_t>(L.units[x].e0 / 4);
+                    int64_t y = x;
+                    int32_t v1 = v0;
+                    while (y < v && (y == x || ((static_cast<int64_t>(L.units[y].e0) + L.units[y].len) / 4 - v0 <=
+                                                        kFlatChunkVectors &&
+                                                    y - x < kFlatChunkUnits))) {
+                        v1 = static_cast<int32_t>((static_cast<int64_t>(L.units[y].e0) + L.units[y].len) / 4);
+                        ++y;
+                    }
+                    L.chunks.push_back(FlatChunk{static_cast<int32_t>(x), v0, v1, static_cast<int32_t>(y)});
+                    x = y;
+                }
+                pz.pad[1] = static_cast<int32_t>(L.chunks.size());
+            }
+            L.pieces.push_back(pz);
             u = v;
         }
         L.piece_start[c + 1] = static_cast<int32_t>(L.pieces.size());
         ub = ue;
+    }
+
+    if (L.flat) {
+        if (L.n_entries / 4 >= (int64_t(1) << 31)) throw std::length_error("too many vectors for a flat layout");
+        L.tailbits.assign(static_cast<size_t>(L.n_entries / 4 / 32 + 2), 0u);
+        for (const Unit& u : L.units) {
+            const int64_t last = (static_cast<int64_t>(u.e0) + u.len) / 4 - 1;
+            L.tailbits[last >> 5] |= 1u << (last & 31);
+        }
     }
 
     // ---- 6. sub-panel split points of the residual pass (entries are ascending within a unit) ---

@@ -81,6 +81,13 @@ struct Piece {
     int32_t pad[3];
 };
 
+// A warp's work item in a flat layout: units [ua, ub) = vectors [v0, v1) (4 entries each).
+struct FlatChunk {
+    int32_t ua, v0, v1, ub;
+};
+constexpr int kFlatChunkVectors = 256;
+constexpr int kFlatChunkUnits = 32;  // a warp holds a chunk's unit descriptors in one register per lane
+
 struct SweepLayout {
     int32_t n_out = 0;        // outputs on this side (local)
     int32_t gat_extent = 0;   // size of the gather index space (padded global space)
@@ -114,6 +121,12 @@ struct SweepLayout {
     int32_t rmw_sub = 1;
     int32_t sub_width = 0;
     std::vector<uint16_t> usplit;     // rmw_sub > 1: per unit rmw_sub+1 entry offsets (0 .. real)
+    // Flat (segmented-stream) layout for short segments (flat_kernels.cu): units in memory order
+    // and contiguous (segments padded to 4 entries, no alignment gaps); warps stream chunks of
+    // whole units; tailbits marks the last 4-entry vector of every unit.
+    bool flat = false;
+    std::vector<FlatChunk> chunks;    // pieces' chunks: Piece::pad[0..1] = chunk range
+    std::vector<uint32_t> tailbits;   // (n_entries / 4) bits + 2 words of slack
 };
 
 // Shared-memory floats one staged vector of `width` occupies (sentinel slot, 16-byte rounded).

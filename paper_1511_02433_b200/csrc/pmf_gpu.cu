@@ -85,6 +85,8 @@ int smem_budget() {
     return b;
 }
 
+constexpr size_t kStreamSlack = 64;  // entries of slack after the residual / index streams
+
 // ---- device memory -----------------------------------------------------------------------------
 struct DevMem {
     std::vector<void*> blocks;
@@ -105,8 +107,8 @@ struct DevMem {
         return p;
     }
     template <class T>
-    T* upload(const PodBuf<T>& v, cudaStream_t s, int64_t* h2d) {
-        T* p = alloc<T>(v.size(), false);
+    T* upload(const PodBuf<T>& v, cudaStream_t s, int64_t* h2d, size_t slack = 0) {
+        T* p = alloc<T>(v.size() + slack, false);
         if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
         if (h2d) *h2d += static_cast<int64_t>(v.size() * sizeof(T));
         return p;
@@ -219,11 +221,17 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     D.n_mo_big = L.n_mo_big;
     D.n_dense = L.n_dense;
     D.avg_segment = L.avg_segment;
+    D.flat = L.flat;
+    if (L.flat) {
+        D.chunks = c.mem.upload(L.chunks, c.stream, &c.h2d);
+        D.tailbits = c.mem.upload(L.tailbits, c.stream, &c.h2d);
+    }
     D.ctas = L.ctas;
     D.n_slots = L.n_slots;
-    if (L.idx16) D.idx = c.mem.upload(L.idx16v, c.stream, &c.h2d);
-    else D.idx = c.mem.upload(L.idx32v, c.stream, &c.h2d);
-    D.R = c.mem.alloc<float>(L.n_entries + 4, false);
+    // slack: the flat kernels load whole 16-entry lane ranges past a layout's last vector (masked)
+    if (L.idx16) D.idx = c.mem.upload(L.idx16v, c.stream, &c.h2d, kStreamSlack);
+    else D.idx = c.mem.upload(L.idx32v, c.stream, &c.h2d, kStreamSlack);
+    D.R = c.mem.alloc<float>(L.n_entries + kStreamSlack, false);
     float* A = c.mem.upload(L.val, c.stream, &c.h2d);
     CUDA_TRY(cudaMemcpyAsync(D.R, A, L.val.size() * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
     *A_copy = A;
@@ -234,7 +242,7 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     {
         std::vector<int32_t> g(4 * L.pieces.size() + 1, 0);
         for (size_t p = 0; p < L.pieces.size(); ++p) {
-            g[4 * p] = L.pieces[p].ub;
+            g[4 * p] = L.flat ? L.pieces[p].pad[0] : L.pieces[p].ub;
             g[4 * p + 1] = L.pieces[p].um;
             g[4 * p + 2] = L.pieces[p].us;
         }
@@ -330,6 +338,7 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     static bool attrs_set = false;
     if (!attrs_set) {
         sweep_set_attributes(kSmemMax + 1024);
+        flat_set_attributes(kSmemMax + 1024);
         als_set_attributes();
         attrs_set = true;
     }
@@ -796,8 +805,8 @@ void get_residual(Ctx& c, float* r_row, float* r_col) {
     const int tp = c.k - 1;
     DevMem tmp;
     DevSweep r = c.csr, q = c.csc;
-    r.R = tmp.alloc<float>(c.csr.n_entries + 4, false);
-    q.R = tmp.alloc<float>(c.csc.n_entries + 4, false);
+    r.R = tmp.alloc<float>(c.csr.n_entries + kStreamSlack, false);
+    q.R = tmp.alloc<float>(c.csc.n_entries + kStreamSlack, false);
     CUDA_TRY(cudaMemcpyAsync(r.R, c.csr.R, c.csr.n_entries * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
     CUDA_TRY(cudaMemcpyAsync(q.R, c.csc.R, c.csc.n_entries * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
     SweepOperands o1;
@@ -939,7 +948,7 @@ pmf_status pmf_ctx_debug_sweep_profile(pmf_ctx* ctx, int32_t side, int32_t promo
         (void)t;
         // work on a copy of R so the training state is untouched
         DevSweep Lc = L;
-        Lc.R = tmp.alloc<float>(L.n_entries + 4, false);
+        Lc.R = tmp.alloc<float>(L.n_entries + kStreamSlack, false);
         CUDA_TRY(cudaMemcpyAsync(Lc.R, L.R, L.n_entries * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
         launch_sweep(Lc, promote ? kPromote : kPlain, side == 0, op, c.stream);
         CUDA_TRY(cudaStreamSynchronize(c.stream));
