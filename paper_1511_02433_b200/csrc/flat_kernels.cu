@@ -53,6 +53,28 @@ template <>
 struct FVar<4> {
     static constexpr int NT = 768, NB = 3;
 };
+// software-pipelined: the next block's loads (across chunk boundaries) are in flight while the
+// current block is processed
+template <>
+struct FVar<5> {
+    static constexpr int NT = 512, NB = 1, PIPE = 1;
+};
+template <>
+struct FVar<6> {
+    static constexpr int NT = 768, NB = 1, PIPE = 1;
+};
+template <>
+struct FVar<7> {
+    static constexpr int NT = 1024, NB = 1, PIPE = 1;
+};
+template <int V, class = void>
+struct IsPipe {
+    static constexpr bool value = false;
+};
+template <int V>
+struct IsPipe<V, decltype(void(FVar<V>::PIPE))> {
+    static constexpr bool value = FVar<V>::PIPE != 0;
+};
 constexpr int kDefaultFlatVariant = 0;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -139,10 +161,14 @@ __device__ __forceinline__ ChunkInfo chunk_info(const FlatChunk& ch, const Unit*
     return ci;
 }
 
+// One 128-vector block of a chunk, its residual / index vectors already loaded into r / ix.
+// cn, cd: the open unit's sum carried across blocks; ucur: unit (relative to the chunk's first)
+// of the block's first valid vector.
 template <int FM, bool CSR>
-__device__ __forceinline__ void flat_chunk(const FlatChunk& ch, const ChunkInfo& ci,
-                                           const uint16_t* __restrict__ idx, float* __restrict__ R,
-                                           float2* __restrict__ partial, const SweepOperands& op, const float* g0) {
+__device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[8], const FlatChunk& ch,
+                                           const ChunkInfo& ci, int vb, float& cn, float& cd, int& ucur,
+                                           float* __restrict__ R, float2* __restrict__ partial,
+                                           const SweepOperands& op, const float* g0) {
     constexpr bool kReduce = FM == kFPlain || FM == kFBuildSweep;
     constexpr bool kWrite = FM != kFPlain;
     const int lane = threadIdx.x & 31;
@@ -152,130 +178,144 @@ __device__ __forceinline__ void flat_chunk(const FlatChunk& ch, const ChunkInfo&
     const float fac = ci.fac;
     const int w0 = v0 >> 5;
     const uint32_t tw = ci.tw;
-    float cn = 0.f, cd = 0.f;  // open unit's sum carried across blocks
-    int ucur = 0;              // unit (relative to ua) of the block's first valid vector
-    for (int vb = v0 & ~3; vb < v1; vb += 128) {
-        const int lv = vb + 4 * lane;
-        float r[16];
-        uint32_t ix[8];
-        const bool any = lv + 3 >= v0 && lv < v1;
-        if (any) {
-            ld8(R + 4 * static_cast<int64_t>(lv), r);
-            ld8(R + 4 * static_cast<int64_t>(lv) + 8, r + 8);
-            ld8u(idx + 4 * static_cast<int64_t>(lv), ix);
-        }
-        uint32_t vmask = 0;
+    const int lv = vb + 4 * lane;
+    const bool any = lv + 3 >= v0 && lv < v1;
+    uint32_t vmask = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) vmask |= (lv + j >= v0 && lv + j < v1) ? (1u << j) : 0u;
-        const uint32_t word = __shfl_sync(0xffffffffu, tw, ((lv >> 5) - w0) & 31);
-        const uint32_t nib = (word >> (lv & 31)) & 0xfu & vmask;
-        const uint32_t b0 = __ballot_sync(0xffffffffu, nib & 1u), b1 = __ballot_sync(0xffffffffu, nib & 2u);
-        const uint32_t b2 = __ballot_sync(0xffffffffu, nib & 4u), b3 = __ballot_sync(0xffffffffu, nib & 8u);
-        int uj = ucur + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
-        const int ul = uj;
-        float pn[4], pd[4];
+    for (int j = 0; j < 4; ++j) vmask |= (lv + j >= v0 && lv + j < v1) ? (1u << j) : 0u;
+    const uint32_t word = __shfl_sync(0xffffffffu, tw, ((lv >> 5) - w0) & 31);
+    const uint32_t nib = (word >> (lv & 31)) & 0xfu & vmask;
+    const uint32_t b0 = __ballot_sync(0xffffffffu, nib & 1u), b1 = __ballot_sync(0xffffffffu, nib & 2u);
+    const uint32_t b2 = __ballot_sync(0xffffffffu, nib & 4u), b3 = __ballot_sync(0xffffffffu, nib & 8u);
+    int uj = ucur + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
+    const int ul = uj;
+    float pn[4], pd[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        pn[j] = pd[j] = 0.f;
+        float fj = 0.f;
+        if (kWrite) fj = __shfl_sync(0xffffffffu, fac, uj & 31);
+        if ((vmask >> j) & 1u) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int e = 4 * j + c;
+                const uint32_t w = ix[e >> 1];
+                const int gi = (e & 1) ? static_cast<int>(w >> 16) : static_cast<int>(w & 0xffffu);
+                const float g = g0[gi];
+                float rr = r[e];
+                if (FM == kFDemote) {
+                    rr = __fsub_rn(rr, __fmul_rn(fj, g));
+                } else if (FM == kFBuild || FM == kFBuildSweep) {
+                    // CSR: w = output factor, h = gathered; CSC: w = gathered, h = output factor
+                    const float wv = CSR ? fj : g;
+                    const float hv = CSR ? g : fj;
+                    if (wv != 0.f) rr = __fadd_rn(rr, __fmul_rn(wv, hv));
+                }
+                if (kReduce) {
+                    pn[j] = fmaf(rr, g, pn[j]);
+                    pd[j] = fmaf(g, g, pd[j]);
+                }
+                r[e] = rr;
+            }
+        }
+        uj += (nib >> j) & 1u;
+    }
+    if (kWrite && any) {
+        if (vmask == 0xfu) {
+            st8(R + 4 * static_cast<int64_t>(lv), r);
+            st8(R + 4 * static_cast<int64_t>(lv) + 8, r + 8);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if ((vmask >> j) & 1u)
+                    __stcs(reinterpret_cast<float4*>(R) + lv + j,
+                           make_float4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
+        }
+    }
+    if (kReduce) {
+        // lane's open sum after its last unit end (all of it if none), and the segmented scan
+        // of those sums: a lane with a unit end starts a new run
+        float vn = 0.f, vd = 0.f;
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-            pn[j] = pd[j] = 0.f;
-            float fj = 0.f;
-            if (kWrite) fj = __shfl_sync(0xffffffffu, fac, uj & 31);
-            if ((vmask >> j) & 1u) {
-#pragma unroll
-                for (int c = 0; c < 4; ++c) {
-                    const int e = 4 * j + c;
-                    const uint32_t w = ix[e >> 1];
-                    const int gi = (e & 1) ? static_cast<int>(w >> 16) : static_cast<int>(w & 0xffffu);
-                    const float g = g0[gi];
-                    float rr = r[e];
-                    if (FM == kFDemote) {
-                        rr = __fsub_rn(rr, __fmul_rn(fj, g));
-                    } else if (FM == kFBuild || FM == kFBuildSweep) {
-                        // CSR: w = output factor, h = gathered; CSC: w = gathered, h = output factor
-                        const float wv = CSR ? fj : g;
-                        const float hv = CSR ? g : fj;
-                        if (wv != 0.f) rr = __fadd_rn(rr, __fmul_rn(wv, hv));
-                    }
-                    if (kReduce) {
-                        pn[j] = fmaf(rr, g, pn[j]);
-                        pd[j] = fmaf(g, g, pd[j]);
-                    }
-                    r[e] = rr;
-                }
-            }
-            uj += (nib >> j) & 1u;
-        }
-        if (kWrite && any) {
-            if (vmask == 0xfu) {
-                st8(R + 4 * static_cast<int64_t>(lv), r);
-                st8(R + 4 * static_cast<int64_t>(lv) + 8, r + 8);
+            if ((nib >> j) & 1u) {
+                vn = 0.f;
+                vd = 0.f;
             } else {
-#pragma unroll
-                for (int j = 0; j < 4; ++j)
-                    if ((vmask >> j) & 1u)
-                        __stcs(reinterpret_cast<float4*>(R) + lv + j,
-                               make_float4(r[4 * j], r[4 * j + 1], r[4 * j + 2], r[4 * j + 3]));
+                vn += pn[j];
+                vd += pd[j];
             }
         }
-        if (kReduce) {
-            // lane's open sum after its last unit end (all of it if none), and the segmented scan
-            // of those sums: a lane with a unit end starts a new run
-            float vn = 0.f, vd = 0.f;
+        // (the sum restarts after each end: vn holds the part after the last end)
+        const uint32_t fm = __ballot_sync(0xffffffffu, nib != 0u);
+        const uint32_t le = fm & (lt | (1u << lane));
+        const int start = le ? 31 - __clz(le) : 0;
+        float in = vn, id = vd;
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                if ((nib >> j) & 1u) {
-                    vn = 0.f;
-                    vd = 0.f;
+        for (int off = 1; off < 32; off <<= 1) {
+            const float n2 = __shfl_up_sync(0xffffffffu, in, off);
+            const float d2 = __shfl_up_sync(0xffffffffu, id, off);
+            if (lane - off >= start) {
+                in += n2;
+                id += d2;
+            }
+        }
+        if (!le) {
+            in += cn;
+            id += cd;
+        }
+        float en = __shfl_up_sync(0xffffffffu, in, 1), ed = __shfl_up_sync(0xffffffffu, id, 1);
+        if (lane == 0) {
+            en = cn;
+            ed = cd;
+        }
+        // walk the lane's vectors from the open sum before it, emitting at every unit end
+        int u = ul;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            en += pn[j];
+            ed += pd[j];
+            const int inf = __shfl_sync(0xffffffffu, info, u & 31);
+            if ((nib >> j) & 1u) {
+                if (inf >= 0) {
+                    partial[inf] = make_float2(en, ed);
                 } else {
-                    vn += pn[j];
-                    vd += pd[j];
+                    const float dt = __fadd_rn(op.lambda, ed);
+                    op.out[op.out_off - inf - 1] = dt == 0.f ? 0.f : __fdiv_rn(en, dt);
                 }
+                en = 0.f;
+                ed = 0.f;
+                ++u;
             }
-            // (the sum restarts after each end: vn holds the part after the last end)
-            const uint32_t fm = __ballot_sync(0xffffffffu, nib != 0u);
-            const uint32_t le = fm & (lt | (1u << lane));
-            const int start = le ? 31 - __clz(le) : 0;
-            float in = vn, id = vd;
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const float n2 = __shfl_up_sync(0xffffffffu, in, off);
-                const float d2 = __shfl_up_sync(0xffffffffu, id, off);
-                if (lane - off >= start) {
-                    in += n2;
-                    id += d2;
-                }
-            }
-            if (!le) {
-                in += cn;
-                id += cd;
-            }
-            float en = __shfl_up_sync(0xffffffffu, in, 1), ed = __shfl_up_sync(0xffffffffu, id, 1);
-            if (lane == 0) {
-                en = cn;
-                ed = cd;
-            }
-            // walk the lane's vectors from the open sum before it, emitting at every unit end
-            int u = ul;
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                en += pn[j];
-                ed += pd[j];
-                const int inf = __shfl_sync(0xffffffffu, info, u & 31);
-                if ((nib >> j) & 1u) {
-                    if (inf >= 0) {
-                        partial[inf] = make_float2(en, ed);
-                    } else {
-                        const float dt = __fadd_rn(op.lambda, ed);
-                        op.out[op.out_off - inf - 1] = dt == 0.f ? 0.f : __fdiv_rn(en, dt);
-                    }
-                    en = 0.f;
-                    ed = 0.f;
-                    ++u;
-                }
-            }
-            cn = __shfl_sync(0xffffffffu, in, 31);
-            cd = __shfl_sync(0xffffffffu, id, 31);
         }
-        ucur += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+        cn = __shfl_sync(0xffffffffu, in, 31);
+        cd = __shfl_sync(0xffffffffu, id, 31);
+    }
+    ucur += __popc(b0) + __popc(b1) + __popc(b2) + __popc(b3);
+}
+
+__device__ __forceinline__ void load_block(float (&r)[16], uint32_t (&ix)[8], const FlatChunk& ch, int vb,
+                                           const uint16_t* __restrict__ idx, const float* __restrict__ R) {
+    const int lv = vb + 4 * (threadIdx.x & 31);
+    if (lv + 3 >= ch.v0 && lv < ch.v1) {
+        ld8(R + 4 * static_cast<int64_t>(lv), r);
+        ld8(R + 4 * static_cast<int64_t>(lv) + 8, r + 8);
+        ld8u(idx + 4 * static_cast<int64_t>(lv), ix);
+    }
+}
+
+// Non-pipelined: one block's loads, then its processing.
+template <int FM, bool CSR>
+__device__ __forceinline__ void flat_chunk(const FlatChunk& ch, const ChunkInfo& ci,
+                                           const uint16_t* __restrict__ idx, float* __restrict__ R,
+                                           float2* __restrict__ partial, const SweepOperands& op, const float* g0) {
+    float cn = 0.f, cd = 0.f;
+    int ucur = 0;
+    for (int vb = ch.v0 & ~3; vb < ch.v1; vb += 128) {
+        float r[16];
+        uint32_t ix[8];
+        load_block(r, ix, ch, vb, idx, R);
+        flat_block<FM, CSR>(r, ix, ch, ci, vb, cn, cd, ucur, R, partial, op, g0);
     }
 }
 
@@ -368,17 +408,62 @@ flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, co
         FlatChunk ch2 = c2 < cend ? chunks[c2] : none;
         if (lane == 0) a = atomicAdd(counter, 1);
         ChunkInfo ci1 = chunk_info<FM>(ch1, units, tb, op);
-        while (c1 < cend) {
-            const ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
-            const int c3 = __shfl_sync(0xffffffffu, a, 0);
-            const FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
+        if constexpr (IsPipe<V>::value) {
+            // (chunk, block) pairs in sequence; the loads of the next pair -- the current chunk's
+            // next block or the next chunk's first -- are issued before the current one is processed
+            ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
+            int c3 = __shfl_sync(0xffffffffu, a, 0);
+            FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
             if (lane == 0) a = atomicAdd(counter, 1);
-            flat_chunk<FM, CSR>(ch1, ci1, idx, R, partial, op, smem);
-            c1 = c2;
-            ch1 = ch2;
-            ci1 = ci2;
-            c2 = c3;
-            ch2 = ch3;
+            float r[16], rn[16];
+            uint32_t ix[8], ixn[8];
+            int vb = ch1.v0 & ~3;
+            if (c1 < cend) load_block(r, ix, ch1, vb, idx, R);
+            float cn = 0.f, cd = 0.f;
+            int ucur = 0;
+            while (c1 < cend) {
+                const int nvb = vb + 128;
+                const bool same = nvb < ch1.v1;
+                if (same) load_block(rn, ixn, ch1, nvb, idx, R);
+                else if (c2 < cend) load_block(rn, ixn, ch2, ch2.v0 & ~3, idx, R);
+                flat_block<FM, CSR>(r, ix, ch1, ci1, vb, cn, cd, ucur, R, partial, op, smem);
+                if (same) {
+                    vb = nvb;
+                } else {
+                    const ChunkInfo ci3 = chunk_info<FM>(ch3, units, tb, op);  // ch3 loaded a chunk ago
+                    const int c4 = __shfl_sync(0xffffffffu, a, 0);
+                    const FlatChunk ch4 = c4 < cend ? chunks[c4] : none;
+                    if (lane == 0) a = atomicAdd(counter, 1);
+                    c1 = c2;
+                    ch1 = ch2;
+                    ci1 = ci2;
+                    c2 = c3;
+                    ch2 = ch3;
+                    ci2 = ci3;
+                    c3 = c4;
+                    ch3 = ch4;
+                    vb = ch1.v0 & ~3;
+                    cn = cd = 0.f;
+                    ucur = 0;
+                }
+#pragma unroll
+                for (int q = 0; q < 16; ++q) r[q] = rn[q];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) ix[q] = ixn[q];
+            }
+        } else {
+            while (c1 < cend) {
+                const ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
+                const int c3 = __shfl_sync(0xffffffffu, a, 0);
+                const FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
+                if (lane == 0) a = atomicAdd(counter, 1);
+                flat_chunk<FM, CSR>(ch1, ci1, idx, R, partial, op, smem);
+                c1 = c2;
+                ch1 = ch2;
+                ci1 = ci2;
+                c2 = c3;
+                ch2 = ch3;
+            }
         }
     }
     if (steal) {
@@ -437,6 +522,9 @@ void launch_flat_mode(const DevSweep& L, const SweepOperands& op, const float* g
         case 2: launch_flat_v<FM, CSR, 2>(L, op, gsrc, steal, s); return;
         case 3: launch_flat_v<FM, CSR, 3>(L, op, gsrc, steal, s); return;
         case 4: launch_flat_v<FM, CSR, 4>(L, op, gsrc, steal, s); return;
+        case 5: launch_flat_v<FM, CSR, 5>(L, op, gsrc, steal, s); return;
+        case 6: launch_flat_v<FM, CSR, 6>(L, op, gsrc, steal, s); return;
+        case 7: launch_flat_v<FM, CSR, 7>(L, op, gsrc, steal, s); return;
         default: launch_flat_v<FM, CSR, 0>(L, op, gsrc, steal, s); return;
     }
 }
@@ -456,6 +544,9 @@ void set_flat_attr(size_t max_smem) {
     set_flat_attr_v<FM, 2>(max_smem);
     set_flat_attr_v<FM, 3>(max_smem);
     set_flat_attr_v<FM, 4>(max_smem);
+    set_flat_attr_v<FM, 5>(max_smem);
+    set_flat_attr_v<FM, 6>(max_smem);
+    set_flat_attr_v<FM, 7>(max_smem);
 }
 
 bool flat_steal() {
