@@ -70,6 +70,9 @@ int launch_flat(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOpe
 void flat_set_attributes(size_t max_smem);
 void sweep_set_attributes(size_t max_smem);
 
+// dst[i * k + t] = src[t * ld + i] for i < count (column-major k x ld factor -> row-major).
+void launch_transpose(const float* src, int64_t ld, int k, int32_t count, float* dst, cudaStream_t stream);
+
 // ---- evaluation (model.hpp:103-167) -----------------------------------------------------------
 // Factor element (i, t) lives at F[i * si + t * st].
 struct FactorView {

@@ -152,4 +152,29 @@ void launch_probe_sse(const DevTriplet* probe, int64_t n, FactorView W, FactorVi
     sum_stage2<<<1, kRedThreads, 0, stream>>>(scratch, kStage1Blocks, out);
 }
 
+// 32 x 32 tiles through shared memory: reads of src rows (fixed t) and writes of dst rows coalesced.
+__global__ void transpose_kernel(const float* __restrict__ src, int64_t ld, int k, int32_t count,
+                                 float* __restrict__ dst) {
+    __shared__ float tile[32][33];
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int t0 = blockIdx.y * 32;
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int t = t0 + y;
+        const int64_t i = i0 + threadIdx.x;
+        if (t < k && i < count) tile[y][threadIdx.x] = src[static_cast<int64_t>(t) * ld + i];
+    }
+    __syncthreads();
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+        const int64_t i = i0 + y;
+        const int t = t0 + threadIdx.x;
+        if (t < k && i < count) dst[i * k + t] = tile[threadIdx.x][y];
+    }
+}
+
+void launch_transpose(const float* src, int64_t ld, int k, int32_t count, float* dst, cudaStream_t stream) {
+    if (count <= 0 || k <= 0) return;
+    const dim3 grid(static_cast<unsigned>((count + 31) / 32), static_cast<unsigned>((k + 31) / 32));
+    transpose_kernel<<<grid, dim3(32, 8), 0, stream>>>(src, ld, k, count, dst);
+}
+
 }  // namespace pmfgpu

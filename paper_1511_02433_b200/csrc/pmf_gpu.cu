@@ -14,6 +14,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
+#include <thread>
 #include <memory>
 #include <random>
 #include <stdexcept>
@@ -87,6 +89,102 @@ int smem_budget() {
 
 constexpr size_t kStreamSlack = 64;  // entries of slack after the residual / index streams
 
+// ---- pinned staging ----------------------------------------------------------------------------
+// Host <-> device copies of large pageable buffers go through two 32 MB pinned buffers: a chunk is
+// memcpy'd into one (host threads) while the other is on the copy engine, which runs at PCIe speed
+// instead of the driver's pageable path (~8 GB/s measured).  Process-wide, allocated on first use.
+struct PinnedStage {
+    static constexpr size_t kChunk = 32u << 20;
+    std::mutex mu;
+    void* buf[2] = {nullptr, nullptr};
+    cudaEvent_t ev[2] = {nullptr, nullptr};
+    int device = -1;
+    void ensure() {
+        int d = 0;
+        CUDA_TRY(cudaGetDevice(&d));
+        if (buf[0] && d == device) return;
+        release();
+        for (int i = 0; i < 2; ++i) {
+            CUDA_TRY(cudaHostAlloc(&buf[i], kChunk, cudaHostAllocDefault));
+            CUDA_TRY(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming));
+        }
+        device = d;
+    }
+    void release() {
+        for (int i = 0; i < 2; ++i) {
+            if (ev[i]) cudaEventDestroy(ev[i]);
+            if (buf[i]) cudaFreeHost(buf[i]);
+            ev[i] = nullptr;
+            buf[i] = nullptr;
+        }
+    }
+};
+PinnedStage& pinned_stage() {
+    static PinnedStage* s = new PinnedStage();  // never destroyed: outlives every context
+    return *s;
+}
+constexpr size_t kStageMin = 4u << 20;  // smaller copies go straight through the driver
+
+void par_memcpy(void* dst, const void* src, size_t bytes) {
+    constexpr int T = 8;
+    std::thread ts[T];
+    for (int t = 0; t < T; ++t) {
+        const size_t o0 = bytes * t / T & ~size_t(63), o1 = t == T - 1 ? bytes : (bytes * (t + 1) / T & ~size_t(63));
+        ts[t] = std::thread([=] {
+            std::memcpy(static_cast<char*>(dst) + o0, static_cast<const char*>(src) + o0, o1 - o0);
+        });
+    }
+    for (auto& t : ts) t.join();
+}
+
+// Host -> device on stream s (returns once the host data has been consumed).
+void staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes < kStageMin) {
+        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
+        return;
+    }
+    PinnedStage& st = pinned_stage();
+    std::lock_guard<std::mutex> lk(st.mu);
+    st.ensure();
+    int i = 0;
+    for (size_t off = 0; off < bytes; off += PinnedStage::kChunk, i ^= 1) {
+        const size_t len = std::min(PinnedStage::kChunk, bytes - off);
+        CUDA_TRY(cudaEventSynchronize(st.ev[i]));  // the buffer's previous copy has finished
+        par_memcpy(st.buf[i], static_cast<const char*>(src) + off, len);
+        CUDA_TRY(cudaMemcpyAsync(static_cast<char*>(dst) + off, st.buf[i], len, cudaMemcpyHostToDevice, s));
+        CUDA_TRY(cudaEventRecord(st.ev[i], s));
+    }
+}
+
+// Device -> host, synchronous (stream s is synchronized).
+void staged_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes < kStageMin) {
+        CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        return;
+    }
+    PinnedStage& st = pinned_stage();
+    std::lock_guard<std::mutex> lk(st.mu);
+    st.ensure();
+    size_t off[2] = {0, 0}, len[2] = {0, 0};
+    int i = 0;
+    auto drain = [&](int b) {
+        if (!len[b]) return;
+        CUDA_TRY(cudaEventSynchronize(st.ev[b]));
+        par_memcpy(static_cast<char*>(dst) + off[b], st.buf[b], len[b]);
+        len[b] = 0;
+    };
+    for (size_t o = 0; o < bytes; o += PinnedStage::kChunk, i ^= 1) {
+        drain(i);
+        off[i] = o;
+        len[i] = std::min(PinnedStage::kChunk, bytes - o);
+        CUDA_TRY(cudaMemcpyAsync(st.buf[i], static_cast<const char*>(src) + o, len[i], cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaEventRecord(st.ev[i], s));
+    }
+    drain(i ^ 1);
+    drain(i);
+}
+
 // ---- device memory -----------------------------------------------------------------------------
 struct DevMem {
     std::vector<void*> blocks;
@@ -102,14 +200,14 @@ struct DevMem {
     template <class T>
     T* upload(const std::vector<T>& v, cudaStream_t s, int64_t* h2d) {
         T* p = alloc<T>(v.size(), false);
-        if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (!v.empty()) staged_h2d(p, v.data(), v.size() * sizeof(T), s);
         if (h2d) *h2d += static_cast<int64_t>(v.size() * sizeof(T));
         return p;
     }
     template <class T>
     T* upload(const PodBuf<T>& v, cudaStream_t s, int64_t* h2d, size_t slack = 0) {
         T* p = alloc<T>(v.size() + slack, false);
-        if (!v.empty()) CUDA_TRY(cudaMemcpyAsync(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s));
+        if (!v.empty()) staged_h2d(p, v.data(), v.size() * sizeof(T), s);
         if (h2d) *h2d += static_cast<int64_t>(v.size() * sizeof(T));
         return p;
     }
@@ -744,7 +842,18 @@ void get_model(Ctx& c, float* W, float* H) {
     if (c.mode == 0) invalid("no model");
     CUDA_TRY(cudaSetDevice(c.device));
     const int k = c.k;
-    if (c.mode == 1) {
+    if (c.mode == 1 && c.world == 1) {
+        // transpose column-major k x ld -> row-major on the device, then a staged download
+        DevMem tmp;
+        float* wt = tmp.alloc<float>(static_cast<size_t>(c.m) * k, false);
+        float* ht = tmp.alloc<float>(static_cast<size_t>(c.n) * k, false);
+        launch_transpose(c.W, c.ldm, k, c.m, wt, c.stream);
+        launch_transpose(c.H, c.ldn, k, c.n, ht, c.stream);
+        if (W) staged_d2h(W, wt, sizeof(float) * c.m * k, c.stream);
+        if (H) staged_d2h(H, ht, sizeof(float) * c.n * k, c.stream);
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        c.d2h += static_cast<int64_t>(sizeof(float) * (static_cast<int64_t>(c.m) + c.n) * k);
+    } else if (c.mode == 1) {
         std::vector<float> w(static_cast<size_t>(k) * c.ldm), h(static_cast<size_t>(k) * c.ldn);
         CUDA_TRY(cudaMemcpy(w.data(), c.W, w.size() * sizeof(float), cudaMemcpyDeviceToHost));
         CUDA_TRY(cudaMemcpy(h.data(), c.H, h.size() * sizeof(float), cudaMemcpyDeviceToHost));
@@ -1032,20 +1141,33 @@ static pmf_status train_common(const pmf_matrix_view* a, int outer, const pmf_tr
         for (int64_t x = 0; x < n_probe; ++x)
             if (probe[x].user < 0 || probe[x].user >= a->m || probe[x].item < 0 || probe[x].item >= a->n)
                 invalid("probe index outside training dimensions");
+        const double t_val = now_s();
         auto c = make_ctx(a, -1, 0, 1, nullptr);
+        const double t_ctx = now_s();
         begin(*c);
         set_probe(*c, probe, n_probe);
-        double train = 0;
+        const double t_begin = now_s();
+        double train = 0, t_iter = 0, t_metrics = 0;
         for (int it = 1; it <= outer; ++it) {
             double s = 0;
+            const double ta = now_s();
             iterate(*c, &s);
+            const double tb = now_s();
             pmf_iter_row& r = rows[it - 1];
             r.iteration = it;
             r.seconds = s;
             metrics(*c, &r.objective, &r.rmse, &r.train_rmse);
+            t_iter += tb - ta;
+            t_metrics += now_s() - tb;
             train += s;
         }
+        const double t_model = now_s();
         get_model(*c, W_out, H_out);
+        if (std::getenv("PMF_VERBOSE"))
+            std::fprintf(stderr,
+                         "[pmf] train: validate %.3f s, context %.3f, begin+probe %.3f, iterate %.3f (device %.3f), "
+                         "metrics %.3f, model download %.3f\n",
+                         t_val - t0, t_ctx - t_val, t_begin - t_ctx, t_iter, train, t_metrics, now_s() - t_model);
         if (totals) {
             totals->train_seconds = train;
             totals->final_objective = rows[outer - 1].objective;
