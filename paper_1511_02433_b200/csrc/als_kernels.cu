@@ -115,6 +115,88 @@ __device__ bool warp_cholesky_solve(float* G, int k, float& b0, float& b1) {
     return true;
 }
 
+// warp_cholesky_solve for k == K known at compile time (the tensor-core kernels' padded order): every
+// loop is unrolled, so the dot products read G with immediate offsets and carry no loop or bounds
+// bookkeeping.  Same arithmetic and order as warp_cholesky_solve.  Opt-in (PMF_ALS_EXACT=1): the
+// unrolled code outgrows the instruction cache and measured 2 % slower at Netflix k = 40.
+template <int K, int GS>
+__device__ __forceinline__ bool warp_cholesky_solve_exact(float* G, float& b0, float& b1) {
+    const int lane = threadIdx.x & 31;
+    bool ok = true;
+#pragma unroll
+    for (int j = 0; j < K; ++j) {
+        const int i0 = j + 1 + lane, i1 = i0 + 32;
+        const bool h0 = i0 < K, h1 = i1 < K;
+        const float* Gj = G + j * GS;
+        const float* G0 = G + (h0 ? i0 : j) * GS;
+        const float* G1 = G + (h1 ? i1 : j) * GS;
+        float d0 = Gj[j], d1 = 0.f, d2 = 0.f, d3 = 0.f;
+        float s0 = h0 ? G0[j] : 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        float r0 = h1 ? G1[j] : 0.f, r1 = 0.f;
+#pragma unroll
+        for (int t = 0; t + 4 <= j; t += 4) {
+            const float g0 = Gj[t], g1 = Gj[t + 1], g2 = Gj[t + 2], g3 = Gj[t + 3];
+            d0 = fmaf(-g0, g0, d0);
+            d1 = fmaf(-g1, g1, d1);
+            d2 = fmaf(-g2, g2, d2);
+            d3 = fmaf(-g3, g3, d3);
+            s0 = fmaf(-G0[t], g0, s0);
+            s1 = fmaf(-G0[t + 1], g1, s1);
+            s2 = fmaf(-G0[t + 2], g2, s2);
+            s3 = fmaf(-G0[t + 3], g3, s3);
+            if (K > 32 && h1) {
+                r0 = fmaf(-G1[t], g0, r0);
+                r1 = fmaf(-G1[t + 1], g1, r1);
+                r0 = fmaf(-G1[t + 2], g2, r0);
+                r1 = fmaf(-G1[t + 3], g3, r1);
+            }
+        }
+#pragma unroll
+        for (int t = j & ~3; t < j; ++t) {
+            const float g0 = Gj[t];
+            d0 = fmaf(-g0, g0, d0);
+            s0 = fmaf(-G0[t], g0, s0);
+            if (K > 32 && h1) r0 = fmaf(-G1[t], g0, r0);
+        }
+        const float d = (d0 + d1) + (d2 + d3);
+        if (!(d > 0.f)) {
+            ok = false;
+            break;
+        }
+        const float ljj = sqrtf(d);
+        const float rl = 1.0f / ljj;
+        __syncwarp();
+        if (h0) G[i0 * GS + j] = ((s0 + s1) + (s2 + s3)) * rl;
+        if (K > 32 && h1) G[i1 * GS + j] = (r0 + r1) * rl;
+        if (lane == 0) G[j * GS + j] = ljj;
+        __syncwarp();
+    }
+    if (!ok) return false;
+#pragma unroll
+    for (int i = 0; i < K; ++i) {
+        const float bi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
+        const float yi = bi / G[i * GS + i];
+        if (lane == (i & 31)) {
+            if (i < 32) b0 = yi;
+            else b1 = yi;
+        }
+        if (lane > i && lane < K) b0 = fmaf(-G[lane * GS + i], yi, b0);
+        if (K > 32 && lane + 32 > i && lane + 32 < K) b1 = fmaf(-G[(lane + 32) * GS + i], yi, b1);
+    }
+#pragma unroll
+    for (int i = K - 1; i >= 0; --i) {
+        const float yi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
+        const float xi = yi / G[i * GS + i];
+        if (lane == (i & 31)) {
+            if (i < 32) b0 = xi;
+            else b1 = xi;
+        }
+        if (lane < i) b0 = fmaf(-G[i * GS + lane], xi, b0);
+        if (K > 32 && lane + 32 < i) b1 = fmaf(-G[i * GS + lane + 32], xi, b1);
+    }
+    return true;
+}
+
 // Stages the gathered opposing rows of one 32-entry chunk into X[s][0..KS): lanes own features
 // (coalesced 4k-byte row reads), 8 rows' loads are issued before they are stored (bank-conflict
 // free stores); columns [k, KS) and rows [cnt, rows_pad) are zero.
@@ -249,7 +331,9 @@ struct TcGeo {
     static constexpr int JN = NT > 2 * MT ? NT : 2 * MT;      // feature slots per lane: g + 8j
     static constexpr int STAGE = 32 * KS;
     static constexpr int GRAM = KMAX * (KMAX + 1) + 2 * KMAX;
-    static constexpr int WARP_FLOATS = (STAGE > GRAM ? STAGE : GRAM) + 64;
+    // staged rows and the gram are separate regions: the rows arrive by TMA bulk copies (async
+    // proxy) and the padding columns of X stay zero for the kernel's lifetime
+    static constexpr int WARP_FLOATS = STAGE + GRAM + 64;
     static constexpr int count_tiles() {
         int c = 0;
         for (int mi = 0; mi < MT; ++mi)
@@ -280,18 +364,31 @@ __global__ void __launch_bounds__(kAlsThreads)
 als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_t* __restrict__ idx,
                    const float* __restrict__ val, const float* __restrict__ opp, float* __restrict__ out,
                    int32_t out_off, int k, float lambda, int weighted, float* __restrict__ partial,
-                   int* __restrict__ counter, int* __restrict__ status) {
+                   int* __restrict__ counter, int* __restrict__ status, int tma, int exact) {
     using T = TcGeo<NT, MT>;
     constexpr int KS = T::KS, JN = T::JN, NTILES = T::NTILES, KMAX = T::KMAX;
     constexpr int GS = KMAX + 1;
     extern __shared__ float smem[];
+    __shared__ __align__(8) uint64_t s_bar[kAlsWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int g = lane >> 2, tig = lane & 3;
     float* X = smem + warp * T::WARP_FLOATS;
-    float* G = X;  // reused after accumulation
+    float* G = X + T::STAGE;
     int* sidx = reinterpret_cast<int*>(X + T::WARP_FLOATS - 64);
     float* sval = X + T::WARP_FLOATS - 32;
+    uint64_t* bar = &s_bar[warp];
+    uint32_t phase = 0;
+    if (tma) {
+        // TMA rows (4k bytes each) leave columns [k, KS) untouched: zero them once
+        for (int e = lane; e < T::STAGE; e += 32) X[e] = 0.f;
+        if (lane == 0) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                static_cast<uint32_t>(__cvta_generic_to_shared(bar))));
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
+        __syncwarp();
+    }
 
     for (;;) {
         int u = 0;
@@ -307,12 +404,45 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
             const int cnt = min(32, U.len - base);
             const int cnt8 = (cnt + 7) & ~7;
             __syncwarp();
-            if (lane < cnt) {
-                sidx[lane] = idx[U.e0 + base + lane];
-                sval[lane] = val[U.e0 + base + lane];
+            if (tma) {
+                // one bulk copy per gathered row, issued by the row's lane, completing on the warp's
+                // mbarrier; the rows past cnt up to the MMA's multiple of 8 are zeroed
+                const int row = lane < cnt ? idx[U.e0 + base + lane] : 0;
+                if (lane < cnt) sval[lane] = val[U.e0 + base + lane];
+                for (int r = cnt; r < cnt8; ++r)
+                    for (int c = lane; c < KS; c += 32) X[r * KS + c] = 0.f;
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                                 "r"(static_cast<uint32_t>(cnt * k * 4))
+                                 : "memory");
+                __syncwarp();
+                if (lane < cnt)
+                    asm volatile(
+                        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                            static_cast<uint32_t>(__cvta_generic_to_shared(X + lane * KS))),
+                        "l"(opp + static_cast<int64_t>(row) * k), "r"(static_cast<uint32_t>(k * 4)), "r"(b)
+                        : "memory");
+                asm volatile(
+                    "{\n"
+                    ".reg .pred p;\n"
+                    "ALSW_%=:\n"
+                    "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                    "@!p bra ALSW_%=;\n"
+                    "}\n" ::"r"(b),
+                    "r"(phase)
+                    : "memory");
+                phase ^= 1;
+            } else {
+                if (lane < cnt) {
+                    sidx[lane] = idx[U.e0 + base + lane];
+                    sval[lane] = val[U.e0 + base + lane];
+                }
+                __syncwarp();
+                stage_rows<KMAX, KS>(X, opp, sidx, cnt, cnt8, k);
             }
-            __syncwarp();
-            stage_rows<KMAX, KS>(X, opp, sidx, cnt, cnt8, k);
             __syncwarp();
             for (int e0 = 0; e0 < cnt8; e0 += 8) {
                 uint32_t hi[JN][2], lo[JN][2];
@@ -382,7 +512,8 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
             continue;
         }
         __syncwarp();
-        const bool ok = warp_cholesky_solve<KMAX>(G, k, rhs0, rhs1);
+        const bool ok = (exact && k == KMAX) ? warp_cholesky_solve_exact<KMAX, GS>(G, rhs0, rhs1)
+                                             : warp_cholesky_solve<KMAX>(G, k, rhs0, rhs1);
         if (!ok) {
             if (lane == 0) atomicExch(status, 4);
             rhs0 = rhs1 = 0.f;
@@ -495,6 +626,11 @@ bool use_tensor_cores() {
     return tc;
 }
 
+bool als_exact_chol() {
+    static const bool on = std::getenv("PMF_ALS_EXACT") != nullptr && std::atoi(std::getenv("PMF_ALS_EXACT")) != 0;
+    return on;
+}
+
 template <int NT, int MT>
 void launch_tc(const DevAls& L, const float* opp, float* out, int32_t out_off, int k, float lambda, bool weighted,
                int* d_counter, int* d_status, int sm_count, cudaStream_t s) {
@@ -502,9 +638,12 @@ void launch_tc(const DevAls& L, const float* opp, float* out, int32_t out_off, i
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_gram_tc_kernel<NT, MT>, kAlsThreads, sm);
     const int blocks = std::max(1, std::min<int>(per_sm * sm_count, (L.n_units + kAlsWarps - 1) / kAlsWarps));
+    // TMA row staging needs 16-byte rows (k % 4 == 0; the factor base is cudaMalloc-aligned)
+    static const bool tma_on = std::getenv("PMF_ALS_TMA") == nullptr || std::atoi(std::getenv("PMF_ALS_TMA")) != 0;
+    const int tma = tma_on && k % 4 == 0 && (reinterpret_cast<uintptr_t>(opp) & 15) == 0 ? 1 : 0;
     als_gram_tc_kernel<NT, MT><<<blocks, kAlsThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off,
                                                                 k, lambda, weighted ? 1 : 0, L.partial, d_counter,
-                                                                d_status);
+                                                                d_status, tma, als_exact_chol() ? 1 : 0);
 }
 
 template <int KMAX>
