@@ -137,12 +137,14 @@ __device__ __forceinline__ void st8(float* p, const float* r) {
 // every unit end), and a segmented scan over the lanes' open sums connects units that span lanes;
 // the open sum at the block end is carried to the next block.  Unit descriptors (packed slot or
 // output; for residual passes the output's factor) sit one per lane and are fetched by shuffles.
-// A chunk's per-lane prologue: its unit descriptors (one per lane) and tail words.
+// A chunk's per-lane prologue: its unit descriptors (one per lane) and tail words.  The raw loaded
+// fields are kept as they are and only combined where they are used (in flat_block), so a warp does
+// not stall on the descriptor loads of the chunk after next while it streams the current one.
 struct ChunkInfo {
-    int info;       // slot >= 0, or -(output + 1) for a direct write
+    int slot;       // the unit's partial slot, or < 0 for a direct write of output o
+    int o;
     float fac;      // residual passes: the unit's output factor
     uint32_t tw;    // tail word w0 + lane
-    float pad;
 };
 
 template <int FM>
@@ -150,14 +152,14 @@ __device__ __forceinline__ ChunkInfo chunk_info(const FlatChunk& ch, const Unit*
                                                 const uint32_t* __restrict__ tb, const SweepOperands& op) {
     constexpr bool kWrite = FM != kFPlain;
     const int lane = threadIdx.x & 31;
-    ChunkInfo ci{0, 0.f, 0u, 0.f};
-    if (lane < ch.ub - ch.ua) {
-        const Unit U = units[ch.ua + lane];
-        ci.info = U.slot >= 0 ? U.slot : -(U.o + 1);
-        if (kWrite) ci.fac = (FM == kFDemote ? op.oa : op.ob)[op.out_off + U.o];
-    }
+    ChunkInfo ci{0, 0, 0.f, 0u};
+    const int ui = min(ch.ua + lane, max(ch.ub - 1, 0));  // clamped: every lane loads (no branch)
+    const int2 so = *reinterpret_cast<const int2*>(&units[ui].o);
+    ci.o = so.x;
+    ci.slot = so.y;
+    if (kWrite) ci.fac = (FM == kFDemote ? op.oa : op.ob)[op.out_off + so.x];
     const int w0 = ch.v0 >> 5;
-    if (ch.v1 > ch.v0 && lane <= ((ch.v1 - 1) >> 5) - w0) ci.tw = __ldg(tb + w0 + lane);
+    ci.tw = __ldg(tb + w0 + min(lane, 9));
     return ci;
 }
 
@@ -174,7 +176,7 @@ __device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int v0 = ch.v0, v1 = ch.v1;
-    const int info = ci.info;
+    const int info = ci.slot >= 0 ? ci.slot : -(ci.o + 1);  // slot, or -(output + 1): direct write
     const float fac = ci.fac;
     const int w0 = v0 >> 5;
     const uint32_t tw = ci.tw;
@@ -319,6 +321,28 @@ __device__ __forceinline__ void flat_chunk(const FlatChunk& ch, const ChunkInfo&
     }
 }
 
+// Chunk claims from a piece's counter, two chunks per atomic; the next pair's atomic is issued when
+// the current pair is first used, so its latency overlaps the streaming of two chunks.
+struct FlatClaim {
+    int* counter;
+    int a;       // outstanding atomic result (lane 0)
+    int second;  // second chunk of the current pair, or -1
+    __device__ __forceinline__ void issue() {
+        if ((threadIdx.x & 31) == 0) a = atomicAdd(counter, 2);
+    }
+    __device__ __forceinline__ int next() {
+        if (second >= 0) {
+            const int c = second;
+            second = -1;
+            return c;
+        }
+        const int b = __shfl_sync(0xffffffffu, a, 0);
+        issue();
+        second = b + 1;
+        return b;
+    }
+};
+
 template <int FM, bool CSR, int V>
 __global__ void __launch_bounds__(FVar<V>::NT, 1)
 flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, const int32_t* __restrict__ piece_start,
@@ -399,16 +423,16 @@ flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, co
         // descriptors / tail words, chunk i+2's descriptor and the claim of chunk i+3 are in flight.
         const int cend = pz.pad[1];
         const FlatChunk none{0, 0, 0, 0};
-        int a = 0;
-        if (lane == 0) a = atomicAdd(counter, 1);
-        int c1 = __shfl_sync(0xffffffffu, a, 0);
-        if (lane == 0) a = atomicAdd(counter, 1);
-        int c2 = __shfl_sync(0xffffffffu, a, 0);
-        FlatChunk ch1 = c1 < cend ? chunks[c1] : none;
-        FlatChunk ch2 = c2 < cend ? chunks[c2] : none;
-        if (lane == 0) a = atomicAdd(counter, 1);
-        ChunkInfo ci1 = chunk_info<FM>(ch1, units, tb, op);
         if constexpr (IsPipe<V>::value) {
+            int a = 0;
+            if (lane == 0) a = atomicAdd(counter, 1);
+            int c1 = __shfl_sync(0xffffffffu, a, 0);
+            if (lane == 0) a = atomicAdd(counter, 1);
+            int c2 = __shfl_sync(0xffffffffu, a, 0);
+            FlatChunk ch1 = c1 < cend ? chunks[c1] : none;
+            FlatChunk ch2 = c2 < cend ? chunks[c2] : none;
+            if (lane == 0) a = atomicAdd(counter, 1);
+            ChunkInfo ci1 = chunk_info<FM>(ch1, units, tb, op);
             // (chunk, block) pairs in sequence; the loads of the next pair -- the current chunk's
             // next block or the next chunk's first -- are issued before the current one is processed
             ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
@@ -452,11 +476,17 @@ flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, co
                 for (int q = 0; q < 8; ++q) ix[q] = ixn[q];
             }
         } else {
+            // chunks are claimed in pairs (one atomic per two chunks), a pair ahead of use
+            FlatClaim cl{counter, 0, -1};
+            cl.issue();
+            int c1 = cl.next(), c2 = cl.next();
+            FlatChunk ch1 = c1 < cend ? chunks[c1] : none;
+            FlatChunk ch2 = c2 < cend ? chunks[c2] : none;
+            ChunkInfo ci1 = chunk_info<FM>(ch1, units, tb, op);
             while (c1 < cend) {
                 const ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
-                const int c3 = __shfl_sync(0xffffffffu, a, 0);
+                const int c3 = cl.next();
                 const FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
-                if (lane == 0) a = atomicAdd(counter, 1);
                 flat_chunk<FM, CSR>(ch1, ci1, idx, R, partial, op, smem);
                 c1 = c2;
                 ch1 = ch2;

@@ -126,7 +126,7 @@ struct SweepLayout {
     // whole units; tailbits marks the last 4-entry vector of every unit.
     bool flat = false;
     std::vector<FlatChunk> chunks;    // pieces' chunks: Piece::pad[0..1] = chunk range
-    std::vector<uint32_t> tailbits;   // (n_entries / 4) bits + 2 words of slack
+    std::vector<uint32_t> tailbits;   // (n_entries / 4) bits + 12 words of slack
 };
 
 // Shared-memory floats one staged vector of `width` occupies (sentinel slot, 16-byte rounded).
