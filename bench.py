@@ -304,6 +304,22 @@ def main():
         o, r, t = ctx.metrics()
         als = {"metric": "sec/outer-iter ALS k=40 Netflix shape", "value": float(np.mean(ts)), "unit": unit,
                "launches_per_iter": ctx.launch_count(), "objective": o, "rmse": r}
+    ingest = None
+    if rank == 0 and not dist:
+        # RatingsMatrix::from_triplets on the GPU vs the host build (same bytes out)
+        import paper_1511_02433_b200 as P
+        tr = res["train"]
+        t0 = time.perf_counter()
+        Ag = P.RatingsMatrix.from_triplets(tr, m, n, device=True)
+        t_gpu = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        Ah = P.RatingsMatrix.from_triplets(tr, m, n)
+        t_host = time.perf_counter() - t0
+        same = all(np.array_equal(getattr(Ag, f), getattr(Ah, f)) for f in
+                   ("row_start", "col_of", "val_row", "col_start", "row_of", "val_col"))
+        ingest = {"from_triplets_gpu_s": round(t_gpu, 3), "from_triplets_host_s": round(t_host, 3),
+                  "host_threads": os.cpu_count(), "bitwise_equal": bool(same), "nnz": int(len(tr))}
+        del Ag, Ah
     e2e = None
     if not args.no_e2e and not dist:
         res["ctx"].close()
@@ -327,7 +343,7 @@ def main():
             "roofline": res["roofline"], "cpu_baseline": cpu, "e2e": e2e,
             "gpu_launches": int(res["launches"] * args.steps), "clocks": res["clocks"],
             "quality": {"objective": res["objective"], "probe_rmse": res["rmse"], "train_rmse": res["train_rmse"]},
-            "per_step_s": res["times"], "als": als}
+            "per_step_s": res["times"], "als": als, "ingest": ingest}
     print(json.dumps(line), flush=True)
 
 

@@ -210,6 +210,12 @@ pmf_status pmf_partition_balanced(const int64_t* costs, int32_t count, int32_t p
 pmf_status pmf_matrix_from_triplets(const pmf_triplet* t, int64_t nnz, int32_t m, int32_t n,
                                     int64_t* row_start, int32_t* col_of, float* val_row,
                                     int64_t* col_start, int32_t* row_of, float* val_col);
+/* The same on the GPU (ingest.cu): staged upload, validation pass, stable radix sorts by (user, item)
+ * and (item, user) keys, offsets + first-duplicate pass, staged download.  Bitwise the same output
+ * and the same errors as pmf_matrix_from_triplets / the reference (nnz < 2^31). */
+pmf_status pmf_matrix_from_triplets_gpu(const pmf_triplet* t, int64_t nnz, int32_t m, int32_t n,
+                                        int64_t* row_start, int32_t* col_of, float* val_row,
+                                        int64_t* col_start, int32_t* row_of, float* val_col);
 /* Synthetic ratings with the recipe of tests/testutil.hpp:91-132 (planted rank + biases + noise,
  * 1..5 stars, uniform users, Zipf(0.8) items, no duplicates), generated per user from
  * independent mt19937 streams so it runs in parallel.  Writes `total` = n_train + n_probe

@@ -129,6 +129,7 @@ _SIGS = {
     "pmf_cholesky_solve_batched": ([C.c_int32, C.c_int32, _P, _P], C.c_int),
     "pmf_partition_balanced": ([_P, C.c_int32, C.c_int32, _P], C.c_int),
     "pmf_matrix_from_triplets": ([_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pmf_matrix_from_triplets_gpu": ([_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
     "pmf_synth_ratings": ([C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_uint32, _P, _P, _P, _P],
                           C.c_int),
     "pmf_nccl_unique_id": ([_P], C.c_int),
@@ -179,6 +180,8 @@ def device_count() -> int:
 
 
 def _as_triplets(t) -> np.ndarray:
+    if isinstance(t, np.ndarray) and t.dtype == TRIPLET and t.flags.c_contiguous:
+        return t  # already the 12-byte Triplet<float> layout: passed zero-copy
     if isinstance(t, np.ndarray) and t.dtype.names and set(("user", "item", "rating")) <= set(t.dtype.names):
         out = np.empty(len(t), TRIPLET)
         out["user"], out["item"], out["rating"] = t["user"], t["item"], t["rating"]
@@ -209,16 +212,17 @@ class RatingsMatrix:
                                  _ptr(self.val_row), _ptr(self.col_start), _ptr(self.row_of), _ptr(self.val_col))
 
     @staticmethod
-    def from_triplets(triplets, m: int, n: int) -> "RatingsMatrix":
-        """Canonical CSR+CSC; IndexError (out_of_range) / ValueError (duplicate, non-finite)."""
+    def from_triplets(triplets, m: int, n: int, device: bool = False) -> "RatingsMatrix":
+        """Canonical CSR+CSC (sparse.hpp:73-149); IndexError (out_of_range) / ValueError (duplicate,
+        non-finite).  device=True builds it on the GPU (pmf_matrix_from_triplets_gpu, bitwise equal)."""
         if m < 0 or n < 0:
             raise ValueError("matrix dimensions must be non-negative")
         t = _as_triplets(triplets)
         nnz = len(t)
-        rs = np.zeros(m + 1, np.int64); co = np.zeros(nnz, np.int32); vr = np.zeros(nnz, np.float32)
-        cs = np.zeros(n + 1, np.int64); ro = np.zeros(nnz, np.int32); vc = np.zeros(nnz, np.float32)
-        _check(lib.pmf_matrix_from_triplets(_ptr(t), nnz, m, n, _ptr(rs), _ptr(co), _ptr(vr), _ptr(cs), _ptr(ro),
-                                            _ptr(vc)))
+        rs = np.empty(m + 1, np.int64); co = np.empty(nnz, np.int32); vr = np.empty(nnz, np.float32)
+        cs = np.empty(n + 1, np.int64); ro = np.empty(nnz, np.int32); vc = np.empty(nnz, np.float32)
+        fn = lib.pmf_matrix_from_triplets_gpu if device else lib.pmf_matrix_from_triplets
+        _check(fn(_ptr(t), nnz, m, n, _ptr(rs), _ptr(co), _ptr(vr), _ptr(cs), _ptr(ro), _ptr(vc)))
         return RatingsMatrix(m, n, rs, co, vr, cs, ro, vc)
 
     def rows(self):

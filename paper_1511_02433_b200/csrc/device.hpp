@@ -91,6 +91,13 @@ struct DevTriplet {
     int32_t user, item;
     float rating;
 };
+// RatingsMatrix::from_triplets (sparse.hpp:73-149) on the device (ingest.cu): CSR + CSC of nnz
+// device triplets into device arrays; *bad = first invalid triplet index or -1, *dup = CSR position of
+// the first duplicate or -1 (outputs valid only when both are -1).  nnz < 2^31.
+size_t ingest_scratch_bytes(int64_t nnz);
+cudaError_t ingest_build(const DevTriplet* t, int64_t nnz, int32_t m, int32_t n, void* scratch, int64_t* row_start,
+                         int32_t* col_of, float* val_row, int64_t* col_start, int32_t* row_of, float* val_col,
+                         int64_t* bad, int64_t* dup, cudaStream_t s);
 // sum over probe of (r - predict)^2, predict in FP32 sequential t (model.hpp:103-114).
 void launch_probe_sse(const DevTriplet* probe, int64_t n, FactorView W, FactorView H, int k,
                       double* scratch, double* out, cudaStream_t stream);

@@ -167,16 +167,18 @@ pmf_status pmf_matrix_from_triplets(const pmf_triplet* t, int64_t nnz, int32_t m
                 }
             }
             for (int64_t p = s + 1; p < f; ++p)
-                if (col_of[p - 1] == col_of[p]) {
+                if (col_of[p - 1] == col_of[p]) {  // first duplicate in row order (sparse.hpp:127-132)
                     int64_t cur = dup_row.load();
-                    while ((cur < 0 || i < cur) && !dup_row.compare_exchange_weak(cur, i)) {
+                    while ((cur < 0 || p < cur) && !dup_row.compare_exchange_weak(cur, p)) {
                     }
                     break;
                 }
         }
     });
     if (dup_row.load() >= 0) {
-        pmfgpu::set_error("duplicate rating for user " + std::to_string(dup_row.load()));
+        const int64_t p = dup_row.load();
+        const int64_t i = std::upper_bound(row_start, row_start + m + 1, p) - row_start - 1;
+        pmfgpu::set_error("duplicate rating for user " + std::to_string(i) + ", item " + std::to_string(col_of[p]));
         return PMF_INVALID_ARGUMENT;
     }
     // CSC mirrored from CSR in ascending row order (sparse.hpp:134-147), per-thread row blocks

@@ -1106,6 +1106,72 @@ pmf_status pmf_ctx_kernel_stats(pmf_ctx* ctx, double* u_ms, int64_t* u_n, double
     });
 }
 
+pmf_status pmf_matrix_from_triplets_gpu(const pmf_triplet* t, int64_t nnz, int32_t m, int32_t n,
+                                        int64_t* row_start, int32_t* col_of, float* val_row, int64_t* col_start,
+                                        int32_t* row_of, float* val_col) {
+    return guard([&] {
+        if (m < 0 || n < 0) invalid("matrix dimensions must be non-negative");
+        if (nnz < 0 || (nnz > 0 && (!t || !col_of || !val_row || !row_of || !val_col)) || !row_start || !col_start)
+            invalid("from_triplets: null buffers");
+        if (nnz >= (int64_t(1) << 31)) invalid("from_triplets_gpu: more than 2^31 - 1 triplets");
+        ensure_device();
+        const double t0 = now_s();
+        cudaStream_t s = nullptr;
+        CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } sg{s};
+        DevMem mem;
+        const size_t N = static_cast<size_t>(nnz > 0 ? nnz : 1);
+        auto* dt = mem.alloc<DevTriplet>(N, false);
+        if (nnz > 0) staged_h2d(dt, t, sizeof(DevTriplet) * static_cast<size_t>(nnz), s);
+        auto* rs = mem.alloc<int64_t>(static_cast<size_t>(m) + 1, false);
+        auto* cs = mem.alloc<int64_t>(static_cast<size_t>(n) + 1, false);
+        auto* co = mem.alloc<int32_t>(N, false);
+        auto* ro = mem.alloc<int32_t>(N, false);
+        auto* vr = mem.alloc<float>(N, false);
+        auto* vc = mem.alloc<float>(N, false);
+        void* scratch = mem.alloc<char>(ingest_scratch_bytes(nnz), false);
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const double t1 = now_s();
+        int64_t bad = -1, dup = -1;
+        CUDA_TRY(ingest_build(dt, nnz, m, n, scratch, rs, co, vr, cs, ro, vc, &bad, &dup, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const double t2 = now_s();
+        if (bad >= 0) {  // the first offending triplet in input order decides (sparse.hpp:82-92)
+            const pmf_triplet& b = t[bad];
+            if (b.user < 0 || b.user >= m)
+                throw PmfError(PMF_OUT_OF_RANGE, "user index " + std::to_string(b.user) + " out of range for m=" +
+                                                     std::to_string(m));
+            if (b.item < 0 || b.item >= n)
+                throw PmfError(PMF_OUT_OF_RANGE, "item index " + std::to_string(b.item) + " out of range for n=" +
+                                                     std::to_string(n));
+            invalid("non-finite rating at user " + std::to_string(b.user));
+        }
+        if (dup >= 0) {  // sparse.hpp:127-132: first duplicate in row order
+            int32_t item = 0;
+            CUDA_TRY(cudaMemcpyAsync(&item, co + dup, sizeof(item), cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaMemcpyAsync(row_start, rs, sizeof(int64_t) * (static_cast<size_t>(m) + 1),
+                                     cudaMemcpyDeviceToHost, s));
+            CUDA_TRY(cudaStreamSynchronize(s));
+            const int64_t i = std::upper_bound(row_start, row_start + m + 1, dup) - row_start - 1;
+            invalid("duplicate rating for user " + std::to_string(i) + ", item " + std::to_string(item));
+        }
+        staged_d2h(row_start, rs, sizeof(int64_t) * (static_cast<size_t>(m) + 1), s);
+        staged_d2h(col_start, cs, sizeof(int64_t) * (static_cast<size_t>(n) + 1), s);
+        if (nnz > 0) {
+            staged_d2h(col_of, co, sizeof(int32_t) * static_cast<size_t>(nnz), s);
+            staged_d2h(val_row, vr, sizeof(float) * static_cast<size_t>(nnz), s);
+            staged_d2h(row_of, ro, sizeof(int32_t) * static_cast<size_t>(nnz), s);
+            staged_d2h(val_col, vc, sizeof(float) * static_cast<size_t>(nnz), s);
+        }
+        if (std::getenv("PMF_VERBOSE"))
+            std::fprintf(stderr, "[pmf] from_triplets_gpu: alloc + upload %.3f s, build %.3f, download %.3f\n", t1 - t0,
+                         t2 - t1, now_s() - t2);
+    });
+}
+
 pmf_status pmf_ctx_layout_info(pmf_ctx* ctx, int32_t side, pmf_layout_info* out) {
     return guard([&] {
         Ctx& c = *as_ctx(ctx);

@@ -57,8 +57,8 @@ def test_from_triplets_errors(pmf):
         pmf.RatingsMatrix.from_triplets([(3, 0, 1.0)], 3, 3)
     with pytest.raises(IndexError):
         pmf.RatingsMatrix.from_triplets([(0, -1, 1.0)], 3, 3)
-    with pytest.raises(ValueError):
-        pmf.RatingsMatrix.from_triplets([(0, 0, 1.0), (0, 0, 2.0)], 3, 3)
+    with pytest.raises(ValueError, match=r"^duplicate rating for user 1, item 2$"):  # sparse.hpp:127-132
+        pmf.RatingsMatrix.from_triplets([(2, 0, 1.0), (1, 2, 1.0), (2, 0, 3.0), (1, 2, 2.0)], 3, 3)
     with pytest.raises(ValueError):
         pmf.RatingsMatrix.from_triplets([(0, 0, float("inf"))], 3, 3)
     with pytest.raises(ValueError):
