@@ -200,6 +200,16 @@ pmf_status pmf_als_solve_rows(const pmf_matrix_view* a, int32_t side, const floa
  * k*k SPD matrices: a is overwritten by L (strict upper zeroed), x by the solution. */
 pmf_status pmf_cholesky_solve_batched(int32_t batch, int32_t k, float* a, float* x);
 
+/* ---- predict path: top_n (model.hpp:172-209) ------------------------------------------------
+ * For each users[u]: the `count` best items of row users[u] of W H^T (row-major m x k / n x k) that
+ * are not in ex_items[ex_start[u] .. ex_start[u+1]) (strictly increasing), by score descending, ties
+ * by ascending item; scores are predict()'s FP32 sums (model.hpp:103-114), bitwise.  out_items /
+ * out_scores are n_users x count (item -1 past out_count[u] = min(count, n - excluded)).
+ * Errors as the reference: count < 1 -> INVALID_ARGUMENT, user outside [0, m) -> OUT_OF_RANGE. */
+pmf_status pmf_top_n(const float* W, const float* H, int32_t m, int32_t n, int32_t k,
+                     const int32_t* users, int32_t n_users, int32_t count, const int64_t* ex_start,
+                     const int32_t* ex_items, int32_t* out_items, float* out_scores, int32_t* out_count);
+
 /* ---- host helpers --------------------------------------------------------------------------- */
 
 /* runtime.hpp:91-136 partition_balanced (bounds has p+1 entries). */

@@ -48,6 +48,9 @@ typedef struct {
                                int64_t* col_start, int32_t* row_of, REAL* val_col,                \
                                int64_t* row_to_col);                                              \
     REAL orc_predict##SUF(const REAL* W, const REAL* H, int k, int32_t i, int32_t j);             \
+    int orc_top_n##SUF(const REAL* W, const REAL* H, int32_t m, int32_t n, int k, int32_t i,      \
+                       int32_t count, const int32_t* rated_sorted, int64_t n_rated,               \
+                       int32_t* out_items, REAL* out_scores);                                     \
     double orc_objective##SUF(int32_t m, int32_t n, int k, const int64_t* row_start,              \
                               const int32_t* col_of, const REAL* val_row, const REAL* W,          \
                               const REAL* H, double lambda, double* loss_out);                    \

@@ -80,6 +80,7 @@ class Oracle:
             getattr(L, "orc_cholesky_solve" + sfx).argtypes = [P, P, C.c_int]
             getattr(L, "orc_gram_add_row_upper" + sfx).argtypes = [P, P, C.c_int]
             getattr(L, "orc_gram_finish" + sfx).argtypes = [P, R, C.c_int]
+            getattr(L, "orc_top_n" + sfx).argtypes = [P, P, I32, I32, C.c_int, I32, I32, P, I64, P, P]
         L.orc_random_triplets.argtypes = [I32, I32, I32, U32, F64, F64, P]
         L.orc_random_triplets.restype = I64
         L.orc_planted_full.argtypes = [I32, I32, C.c_int, F64, U32, P]
@@ -256,6 +257,21 @@ class Oracle:
         return x
 
 
+    def top_n(self, W, H, i, count, rated=(), real="_f32"):
+        """model.hpp:172-198; returns [(item, score)] or raises like the reference."""
+        npr, R, _ = real_of(real)
+        W = np.ascontiguousarray(W, npr); H = np.ascontiguousarray(H, npr)
+        m, k = W.shape; n = H.shape[0]
+        r = np.ascontiguousarray(rated, np.int32)
+        items = np.zeros(max(count, 1), np.int32); scores = np.zeros(max(count, 1), npr)
+        kept = getattr(self.lib, "orc_top_n" + real)(ptr(W), ptr(H), m, n, k, i, count, ptr(r), len(r),
+                                                      ptr(items), ptr(scores))
+        if kept == -1:
+            raise ValueError("count must be >= 1")
+        if kept == -2:
+            raise IndexError("user index out of range")
+        return [(int(items[x]), scores[x]) for x in range(kept)]
+
 class Reference:
     """The reference itself (parmf headers compiled in place), through ref_driver.cpp."""
 
@@ -286,6 +302,7 @@ class Reference:
             getattr(L, "ref_cholesky_solve" + sfx).argtypes = [P, P, C.c_int]
             getattr(L, "ref_ccdpp_sample" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, C.c_int, U64, P]
             getattr(L, "ref_als_sample" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, U64, P]
+            getattr(L, "ref_top_n" + sfx).argtypes = [P, P, I32, I32, C.c_int, I32, I32, P, I64, P, P, P]
         L.ref_synth_ratings.argtypes = [I32, I32, C.c_int, I64, U32, P]
         L.ref_synth_ratings.restype = I64
         L.ref_random_triplets.argtypes = [I32, I32, C.c_int, U32, F64, F64, P]
@@ -363,6 +380,17 @@ class Reference:
         self._check(getattr(self.lib, "ref_cholesky_solve" + real)(ptr(l), ptr(x), l.shape[0]))
         return x
 
+
+    def top_n(self, W, H, i, count, rated=(), real="_f32"):
+        npr, R, _ = real_of(real)
+        W = np.ascontiguousarray(W, npr); H = np.ascontiguousarray(H, npr)
+        m, k = W.shape; n = H.shape[0]
+        r = np.ascontiguousarray(rated, np.int32)
+        items = np.zeros(max(count, 1), np.int32); scores = np.zeros(max(count, 1), npr)
+        kept = C.c_int32()
+        self._check(getattr(self.lib, "ref_top_n" + real)(ptr(W), ptr(H), m, n, k, i, count, ptr(r), len(r),
+                                                          ptr(items), ptr(scores), C.byref(kept)))
+        return [(int(items[x]), scores[x]) for x in range(kept.value)]
 
 class RefMatrix:
     """parmf::RatingsMatrix<Real> owned by the reference library."""

@@ -127,6 +127,23 @@ const char* ref_last_error() { return g_err; }
             *out = objective(model, a, lambda);                                                     \
         })                                                                                          \
     }                                                                                               \
+    /* model.hpp:172-198 top_n through the reference's own function; returns the kept count */    \
+    int ref_top_n##SUF(const Real* W, const Real* H, int32_t m, int32_t n, int k, int32_t i,        \
+                       int32_t count, const int32_t* rated, int64_t n_rated, int32_t* out_items,    \
+                       Real* out_scores, int32_t* kept) {                                           \
+        GUARD({                                                                                     \
+            FactorModel<Real> model(m, n, k);                                                       \
+            std::copy(W, W + model.w().size(), model.w().begin());                                  \
+            std::copy(H, H + model.h().size(), model.h().begin());                                  \
+            std::vector<index_t> r(rated, rated + n_rated);                                         \
+            const auto best = top_n(model, i, count, std::span<const index_t>(r));                  \
+            for (size_t x = 0; x < best.size(); ++x) {                                              \
+                out_items[x] = best[x].first;                                                       \
+                out_scores[x] = best[x].second;                                                     \
+            }                                                                                       \
+            *kept = static_cast<int32_t>(best.size());                                              \
+        })                                                                                          \
+    }                                                                                               \
     int ref_rmse##SUF(const Real* W, const Real* H, int32_t m, int32_t n, int k,                    \
                       const RefTriplet<Real>* probe, int64_t P, double* out) {                      \
         GUARD({                                                                                     \

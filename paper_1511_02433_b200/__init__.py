@@ -44,6 +44,7 @@ __all__ = [
     "predict", "init_random_items", "ccdpp_build_rhat", "ccdpp_update_u", "ccdpp_update_v", "ccdpp_writeback",
     "solve_user_rows", "solve_item_rows", "cholesky_solve_batched", "partition_balanced", "synth_ratings",
     "Context", "DataError", "NotPositiveDefinite", "DomainError", "device_count", "nccl_unique_id", "dist_plan",
+    "top_n", "top_n_batch",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -130,6 +131,7 @@ _SIGS = {
     "pmf_partition_balanced": ([_P, C.c_int32, C.c_int32, _P], C.c_int),
     "pmf_matrix_from_triplets": ([_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
     "pmf_matrix_from_triplets_gpu": ([_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pmf_top_n": ([_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P], C.c_int),
     "pmf_synth_ratings": ([C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_uint32, _P, _P, _P, _P],
                           C.c_int),
     "pmf_nccl_unique_id": ([_P], C.c_int),
@@ -605,6 +607,54 @@ def nccl_unique_id() -> bytes:
     buf = (C.c_uint8 * 128)()
     _check(lib.pmf_nccl_unique_id(buf))
     return bytes(buf)
+
+
+def top_n_batch(model: FactorModel, users, count: int, a: "RatingsMatrix" = None, rated=None):
+    """model.hpp:172-209 for a batch of users on the B200 (pmf_top_n): the `count` best unrated items
+    of each user, score descending, ties by ascending item; scores bitwise predict()'s.  Exclusions:
+    the users' rows of `a` (the matrix overload), or `rated` = one strictly increasing list per user.
+    Returns (items [len(users), count] with -1 past the end, scores, counts)."""
+    users = np.ascontiguousarray(users, np.int32)
+    nu = len(users)
+    if count < 1:
+        raise ValueError("count must be >= 1")  # model.hpp:175, checked before the user (:176-177)
+    if nu and (users.min() < 0 or users.max() >= model.users()):
+        raise IndexError("user index out of range")
+    if a is not None:
+        if rated is not None:
+            raise ValueError("pass either a or rated")
+        lo = a.row_start[users] if nu else np.zeros(0, np.int64)
+        ln = (a.row_start[users + 1] - lo) if nu else np.zeros(0, np.int64)
+        ex_start = np.concatenate([[0], np.cumsum(ln)]).astype(np.int64)
+        # gather the users' rows in one vectorised index: position p of user u -> lo[u] + (p - ex_start[u])
+        pos = np.repeat(lo - ex_start[:-1], ln) + np.arange(int(ex_start[-1]), dtype=np.int64)
+        ex = a.col_of[pos]
+    else:
+        lists = [np.asarray(r, np.int32) for r in (rated if rated is not None else [()] * nu)]
+        if len(lists) != nu:
+            raise ValueError("one rated list per user")
+        ex_start = np.concatenate([[0], np.cumsum([len(r) for r in lists])]).astype(np.int64)
+        ex = np.concatenate(lists).astype(np.int32) if lists else np.zeros(0, np.int32)
+    ex = np.ascontiguousarray(ex, np.int32) if len(ex) else np.zeros(1, np.int32)
+    W = np.ascontiguousarray(model.w, np.float32); H = np.ascontiguousarray(model.h, np.float32)
+    c = max(int(count), 1)
+    items = np.empty((nu, c), np.int32); scores = np.empty((nu, c), np.float32); counts = np.empty(nu, np.int32)
+    _check(lib.pmf_top_n(_ptr(W), _ptr(H), W.shape[0], H.shape[0], W.shape[1], _ptr(users), nu, int(count),
+                         _ptr(ex_start), _ptr(ex), _ptr(items), _ptr(scores), _ptr(counts)))
+    return items, scores, counts
+
+
+def top_n(model: FactorModel, *args):
+    """The reference's two overloads (model.hpp:172, :203): top_n(model, i, count, rated_sorted) and
+    top_n(model, a, i, count) -> [(item, score)], computed on the B200."""
+    if args and isinstance(args[0], RatingsMatrix):
+        a, i, count = args
+        items, scores, counts = top_n_batch(model, [i], count, a=a)
+    else:
+        i, count = args[0], args[1]
+        rated = args[2] if len(args) > 2 else ()
+        items, scores, counts = top_n_batch(model, [i], count, rated=[rated])
+    return [(int(items[0, x]), float(scores[0, x])) for x in range(counts[0])]
 
 
 # ---------------------------------------------------------------------------------------------

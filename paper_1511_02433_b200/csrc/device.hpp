@@ -102,6 +102,16 @@ cudaError_t ingest_build(const DevTriplet* t, int64_t nnz, int32_t m, int32_t n,
 void launch_probe_sse(const DevTriplet* probe, int64_t n, FactorView W, FactorView H, int k,
                       double* scratch, double* out, cudaStream_t stream);
 
+// ---- top_n (model.hpp:172-209), topn_kernels.cu ------------------------------------------------
+// For each of n_users users (W rows users[u]): the `count` best unrated items of W H^T (row-major
+// m x k, n x k), excluding ex_items[ex_start[u] .. ex_start[u+1]) (ascending).  out_* are
+// n_users x count (items -1 past out_count[u]).
+size_t topn_smem_bytes(int k, int count);
+void topn_set_attributes(size_t max_smem);
+void launch_topn(const float* W, const float* H, int32_t n, int k, const int32_t* users, int32_t n_users,
+                 const int64_t* ex_start, const int32_t* ex_items, int count, int32_t* out_items, float* out_scores,
+                 int32_t* out_count, cudaStream_t s);
+
 // ---- ALS (als.hpp:47-68, dense.hpp:35-124) ------------------------------------------------------
 struct DevAls {
     int32_t n_out = 0, n_units = 0, n_mo = 0, n_slots = 0, n_empty = 0;

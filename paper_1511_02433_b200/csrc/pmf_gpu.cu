@@ -1172,6 +1172,75 @@ pmf_status pmf_matrix_from_triplets_gpu(const pmf_triplet* t, int64_t nnz, int32
     });
 }
 
+pmf_status pmf_top_n(const float* W, const float* H, int32_t m, int32_t n, int32_t k, const int32_t* users,
+                     int32_t n_users, int32_t count, const int64_t* ex_start, const int32_t* ex_items,
+                     int32_t* out_items, float* out_scores, int32_t* out_count) {
+    return guard([&] {
+        if (count < 1) invalid("count must be >= 1");  // model.hpp:175
+        if (m < 0 || n < 0 || k < 1 || n_users < 0) invalid("invalid dimensions");
+        if (n_users > 0 && (!users || !ex_start || !out_items || !out_scores || !out_count)) invalid("null buffers");
+        if ((m > 0 && !W) || (n > 0 && !H)) invalid("null factors");
+        for (int32_t u = 0; u < n_users; ++u)
+            if (users[u] < 0 || users[u] >= m) throw PmfError(PMF_OUT_OF_RANGE, "user index out of range");
+        if (n_users > 0 && ex_start[0] != 0) invalid("exclusion offsets must start at 0");
+        for (int32_t u = 0; u < n_users; ++u) {
+            if (ex_start[u + 1] < ex_start[u]) invalid("exclusion offsets must be non-decreasing");
+            for (int64_t p = ex_start[u] + 1; p < ex_start[u + 1]; ++p)
+                if (ex_items[p] <= ex_items[p - 1]) invalid("rated items must be strictly increasing");
+        }
+        const size_t smem = topn_smem_bytes(k, count);
+        constexpr size_t kTopnSmemMax = 224 * 1024;  // + the kernel's static shared memory <= 227 KB
+        if (smem > kTopnSmemMax) invalid("top_n on the GPU: k x count too large for shared memory (k " +
+                                       std::to_string(k) + ", count " + std::to_string(count) + ")");
+        if (n_users == 0) return;
+        ensure_device();
+        static bool attr = false;
+        if (!attr) {
+            topn_set_attributes(kTopnSmemMax);
+            attr = true;
+        }
+        cudaStream_t s = nullptr;
+        CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+        struct StreamGuard {
+            cudaStream_t s;
+            ~StreamGuard() { cudaStreamDestroy(s); }
+        } sg{s};
+        DevMem mem;
+        const int64_t n_ex = ex_start[n_users];
+        float* dW = mem.alloc<float>(static_cast<size_t>(m) * k, false);
+        float* dH = mem.alloc<float>(static_cast<size_t>(n) * k, false);
+        int32_t* du = mem.alloc<int32_t>(n_users, false);
+        int64_t* des = mem.alloc<int64_t>(static_cast<size_t>(n_users) + 1, false);
+        int32_t* dex = mem.alloc<int32_t>(static_cast<size_t>(std::max<int64_t>(n_ex, 1)), false);
+        int32_t* doi = mem.alloc<int32_t>(static_cast<size_t>(n_users) * count, false);
+        float* dos = mem.alloc<float>(static_cast<size_t>(n_users) * count, false);
+        int32_t* doc = mem.alloc<int32_t>(n_users, false);
+        staged_h2d(dW, W, sizeof(float) * static_cast<size_t>(m) * k, s);
+        staged_h2d(dH, H, sizeof(float) * static_cast<size_t>(n) * k, s);
+        staged_h2d(du, users, sizeof(int32_t) * n_users, s);
+        staged_h2d(des, ex_start, sizeof(int64_t) * (static_cast<size_t>(n_users) + 1), s);
+        if (n_ex > 0) staged_h2d(dex, ex_items, sizeof(int32_t) * static_cast<size_t>(n_ex), s);
+        cudaEvent_t e0, e1;
+        CUDA_TRY(cudaEventCreate(&e0));
+        CUDA_TRY(cudaEventCreate(&e1));
+        CUDA_TRY(cudaEventRecord(e0, s));
+        launch_topn(dW, dH, n, k, du, n_users, des, dex, count, doi, dos, doc, s);
+        CUDA_TRY(cudaEventRecord(e1, s));
+        CUDA_TRY(cudaGetLastError());
+        if (std::getenv("PMF_VERBOSE")) {
+            CUDA_TRY(cudaEventSynchronize(e1));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, e0, e1);
+            std::fprintf(stderr, "[pmf] top_n: %d users, kernel %.3f ms\n", n_users, ms);
+        }
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        staged_d2h(out_items, doi, sizeof(int32_t) * static_cast<size_t>(n_users) * count, s);
+        staged_d2h(out_scores, dos, sizeof(float) * static_cast<size_t>(n_users) * count, s);
+        staged_d2h(out_count, doc, sizeof(int32_t) * n_users, s);
+    });
+}
+
 pmf_status pmf_ctx_layout_info(pmf_ctx* ctx, int32_t side, pmf_layout_info* out) {
     return guard([&] {
         Ctx& c = *as_ctx(ctx);

@@ -1,0 +1,34 @@
+"""Wall time of top_n_batch (pmf_top_n, copies included) for every user of the Netflix-shape matrix
+(k=40, count=10, rated items excluded) next to the reference's top_n on a sample of users."""
+import os
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import bench  # noqa: E402
+import paper_1511_02433_b200 as P  # noqa: E402
+
+train, probe, A = bench.make_data("netflix-ccdpp")
+rng = np.random.default_rng(1)
+model = P.FactorModel(rng.normal(0, 0.3, (A.m, 40)).astype(np.float32), rng.normal(0, 0.3, (A.n, 40)).astype(np.float32))
+users = np.arange(A.m, dtype=np.int32)
+P.top_n_batch(model, users[:1000], 10, a=A)  # warm-up
+for rep in range(2):
+    t0 = time.perf_counter()
+    items, scores, counts = P.top_n_batch(model, users, 10, a=A)
+    print(f"top_n_batch all {A.m} users: {time.perf_counter() - t0:.3f} s", file=sys.stderr)
+try:
+    from oracle.pyoracle import Reference
+    R = Reference()
+    t0 = time.perf_counter()
+    for i in range(200):
+        rated = A.col_of[A.row_start[i]:A.row_start[i + 1]]
+        ref = R.top_n(model.w, model.h, i, 10, rated)
+        assert [j for j, _ in ref] == list(items[i, :10])
+    dt = time.perf_counter() - t0
+    print(f"reference top_n: {dt / 200 * 1e3:.2f} ms/user (1 thread) -> {dt / 200 * A.m:.1f} s for all users", file=sys.stderr)
+except Exception as e:
+    print("reference unavailable:", e, file=sys.stderr)
