@@ -111,6 +111,10 @@ pmf_status pmf_ccdpp_train(const pmf_ccd_config* config, const pmf_matrix_view* 
                            pmf_iter_row* rows_out, pmf_train_totals* totals_out);
 
 /* als.hpp:188-233 als_train<float>. */
+/* ccd.hpp:310-344 ccd_train (CcdVariant::kCcd): same inputs / outputs as pmf_ccdpp_train. */
+pmf_status pmf_ccd_train(const pmf_ccd_config* config, const pmf_matrix_view* a,
+                         const pmf_triplet* probe, int64_t n_probe, float* W_out, float* H_out,
+                         pmf_iter_row* rows_out, pmf_train_totals* totals_out);
 pmf_status pmf_als_train(const pmf_als_config* config, const pmf_matrix_view* a,
                          const pmf_triplet* probe, int64_t n_probe, float* W_out, float* H_out,
                          pmf_iter_row* rows_out, pmf_train_totals* totals_out);
@@ -138,6 +142,10 @@ pmf_status pmf_ctx_ccdpp_begin(pmf_ctx* ctx, const pmf_ccd_config* config);
 pmf_status pmf_ctx_ccdpp_iterate(pmf_ctx* ctx, int32_t n_outer, double* iter_seconds);
 
 /* ALS: W = 0, H = init_random_items(seed). */
+/* Item/user-wise CCD (ccd.hpp:52-125, ccd_train :310-344; inner_iters validated and ignored);
+ * one device only.  ccd_iterate runs whole epochs (W sweep, then H sweep). */
+pmf_status pmf_ctx_ccd_begin(pmf_ctx* ctx, const pmf_ccd_config* config);
+pmf_status pmf_ctx_ccd_iterate(pmf_ctx* ctx, int32_t n_outer, double* iter_seconds);
 pmf_status pmf_ctx_als_begin(pmf_ctx* ctx, const pmf_als_config* config);
 pmf_status pmf_ctx_als_iterate(pmf_ctx* ctx, int32_t n_outer, double* iter_seconds);
 

@@ -66,6 +66,11 @@ typedef struct {
     void orc_ccdpp_writeback##SUF(int32_t m, int32_t n, int k, int t, const int64_t* row_start,   \
                                   const int32_t* col_of, const int64_t* row_to_col, REAL* r_row,  \
                                   REAL* r_col, REAL* W, REAL* H, const REAL* u, const REAL* v);   \
+    int orc_ccd_train##SUF(int k, REAL lambda, int outer, uint64_t seed, int32_t m, int32_t n,     \
+                           const int64_t* row_start, const int32_t* col_of, const REAL* val_row,  \
+                           const int64_t* col_start, const int32_t* row_of, const REAL* val_col,  \
+                           const int64_t* row_to_col, const orc_triplet##SUF* probe, int64_t P,   \
+                           REAL* W, REAL* H, orc_iter_row* rows);                                 \
     int orc_ccdpp_train##SUF(int k, REAL lambda, int outer, int inner, uint64_t seed, int32_t m,  \
                              int32_t n, const int64_t* row_start, const int32_t* col_of,          \
                              const REAL* val_row, const int64_t* col_start,                       \

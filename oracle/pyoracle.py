@@ -81,6 +81,8 @@ class Oracle:
             getattr(L, "orc_gram_add_row_upper" + sfx).argtypes = [P, P, C.c_int]
             getattr(L, "orc_gram_finish" + sfx).argtypes = [P, R, C.c_int]
             getattr(L, "orc_top_n" + sfx).argtypes = [P, P, I32, I32, C.c_int, I32, I32, P, I64, P, P]
+            getattr(L, "orc_ccd_train" + sfx).argtypes = [C.c_int, R, C.c_int, U64, I32, I32, P, P, P, P, P, P, P,
+                                                          P, I64, P, P, P]
         L.orc_random_triplets.argtypes = [I32, I32, I32, U32, F64, F64, P]
         L.orc_random_triplets.restype = I64
         L.orc_planted_full.argtypes = [I32, I32, C.c_int, F64, U32, P]
@@ -162,6 +164,20 @@ class Oracle:
         if rc:
             raise ValueError("probe set is empty")
         return float(out[0])
+
+    def ccd_train(self, A, k, lam, outer, seed, probe=None, real="_f32"):
+        """ccd.hpp:310-344 item/user-wise CCD (restated)."""
+        dt, _, td = real_of(real)
+        pr = np.zeros(0, td) if probe is None else np.ascontiguousarray(np.asarray(probe).astype(td))
+        W = np.zeros((A.m, k), dt); H = np.zeros((A.n, k), dt)
+        rows = np.zeros(outer, ITER_ROW)
+        rc = getattr(self.lib, "orc_ccd_train" + real)(
+            k, lam, outer, seed, A.m, A.n, ptr(A.row_start), ptr(A.col_of), ptr(A.val_row),
+            ptr(A.col_start), ptr(A.row_of), ptr(A.val_col), ptr(A.xlink), ptr(pr), len(pr),
+            ptr(W), ptr(H), ptr(rows))
+        if rc:
+            raise ValueError("invalid CCD configuration or probe")
+        return W, H, rows
 
     def ccdpp_train(self, A, k, lam, outer, inner, seed, probe=None, real="_f32"):
         dt, _, td = real_of(real)
@@ -303,6 +319,7 @@ class Reference:
             getattr(L, "ref_ccdpp_sample" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, C.c_int, U64, P]
             getattr(L, "ref_als_sample" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, U64, P]
             getattr(L, "ref_top_n" + sfx).argtypes = [P, P, I32, I32, C.c_int, I32, I32, P, I64, P, P, P]
+            getattr(L, "ref_ccd_train" + sfx).argtypes = [P, C.c_int, R, C.c_int, U64, P, I64, P, P, P]
         L.ref_synth_ratings.argtypes = [I32, I32, C.c_int, I64, U32, P]
         L.ref_synth_ratings.restype = I64
         L.ref_random_triplets.argtypes = [I32, I32, C.c_int, U32, F64, F64, P]
@@ -439,6 +456,15 @@ class RefMatrix:
         rows = np.zeros(outer, ITER_ROW); ts = np.zeros(1)
         self.ref._check(getattr(self.ref.lib, "ref_ccdpp_train" + self.real)(
             self.h, k, lam, outer, inner, workers, seed, ptr(pr), len(pr), ptr(W), ptr(H), ptr(rows), ptr(ts)))
+        return W, H, rows
+
+    def ccd_train(self, k, lam, outer, seed, probe=None):
+        dt, _, _ = real_of(self.real)
+        pr = self._probe(probe)
+        W = np.zeros((self.m, k), dt); H = np.zeros((self.n, k), dt)
+        rows = np.zeros(outer, ITER_ROW)
+        self.ref._check(getattr(self.ref.lib, "ref_ccd_train" + self.real)(
+            self.h, k, lam, outer, seed, ptr(pr), len(pr), ptr(W), ptr(H), ptr(rows)))
         return W, H, rows
 
     def ccdpp_stage_loop(self, k, lam, outer, inner, seed, probe=None, workers=1):

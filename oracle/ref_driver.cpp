@@ -172,6 +172,23 @@ const char* ref_last_error() { return g_err; }
             *train_seconds = rep.train_seconds;                                                     \
         })                                                                                          \
     }                                                                                               \
+    /* ccd.hpp:310-344 item/user-wise ccd_train through the reference's own entry point */         \
+    int ref_ccd_train##SUF(void* h, int k, Real lambda, int outer, uint64_t seed,                   \
+                           const RefTriplet<Real>* probe, int64_t P, Real* W, Real* H,              \
+                           IterRow* rows) {                                                         \
+        GUARD({                                                                                     \
+            const auto& a = static_cast<MatrixHandle<Real>*>(h)->a;                                 \
+            CcdConfig<Real> c;                                                                      \
+            c.k = k; c.lambda = lambda; c.outer_iters = outer; c.variant = CcdVariant::kCcd;       \
+            c.seed = seed;                                                                          \
+            const auto pr = to_trips(probe, P);                                                     \
+            auto [model, rep] = ccd_train(c, a, std::span<const Triplet<Real>>(pr));                \
+            copy_model(model, W, H);                                                                \
+            for (size_t i = 0; i < rep.rows.size(); ++i)                                            \
+                rows[i] = {rep.rows[i].iteration, rep.rows[i].seconds, rep.rows[i].objective,       \
+                           rep.rows[i].rmse, NAN};                                                  \
+        })                                                                                          \
+    }                                                                                               \
     /* stage-API loop (tests/acceptance_test.cpp:150-171 pattern): same schedule as ccdpp_train, */ \
     /* plus per-iteration train RMSE and the final residual in both layouts */                     \
     int ref_ccdpp_stage_loop##SUF(void* h, int k, Real lambda, int outer, int inner, int workers,   \

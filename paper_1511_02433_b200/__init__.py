@@ -44,7 +44,7 @@ __all__ = [
     "predict", "init_random_items", "ccdpp_build_rhat", "ccdpp_update_u", "ccdpp_update_v", "ccdpp_writeback",
     "solve_user_rows", "solve_item_rows", "cholesky_solve_batched", "partition_balanced", "synth_ratings",
     "Context", "DataError", "NotPositiveDefinite", "DomainError", "device_count", "nccl_unique_id", "dist_plan",
-    "top_n", "top_n_batch",
+    "top_n", "top_n_batch", "ccd_train",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -103,6 +103,9 @@ _SIGS = {
     "pmf_device_count": ([], C.c_int32),
     "pmf_ccdpp_train": ([_P, _P, _P, C.c_int64, _P, _P, _P, _P], C.c_int),
     "pmf_als_train": ([_P, _P, _P, C.c_int64, _P, _P, _P, _P], C.c_int),
+    "pmf_ccd_train": ([_P, _P, _P, C.c_int64, _P, _P, _P, _P], C.c_int),
+    "pmf_ctx_ccd_begin": ([_P, _P], C.c_int),
+    "pmf_ctx_ccd_iterate": ([_P, C.c_int32, _P], C.c_int),
     "pmf_rmse": ([_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64, _P], C.c_int),
     "pmf_objective": ([_P, _P, _P, C.c_int32, C.c_double, _P], C.c_int),
     "pmf_ctx_create": ([_P, C.c_int32, _P], C.c_int),
@@ -443,6 +446,18 @@ def ccdpp_train(config: CcdConfig, a: RatingsMatrix, probe=None):
     return FactorModel(W, H), _report("ccdpp", config, a, rows, tot, config.inner_iters)
 
 
+def ccd_train(config: CcdConfig, a: RatingsMatrix, probe=None):
+    """ccd.hpp:310-344 item/user-wise CCD -> (FactorModel, TrainReport) computed on the B200 (one device;
+    inner_iters is ignored, as in the reference)."""
+    config.validate()
+    pr = _probe_arr(probe)
+    W = np.zeros((a.m, config.k), np.float32); H = np.zeros((a.n, config.k), np.float32)
+    rows = np.zeros(config.outer_iters, _ITER); tot = _Totals()
+    cfg = config._c()
+    _check(lib.pmf_ccd_train(C.byref(cfg), a.view(), _ptr(pr), len(pr), _ptr(W), _ptr(H), _ptr(rows), C.byref(tot)))
+    return FactorModel(W, H), _report("ccd", config, a, rows, tot, 1)
+
+
 def als_train(config: AlsConfig, a: RatingsMatrix, probe=None):
     """als.hpp:188-233 -> (FactorModel, TrainReport) computed on the B200."""
     config.validate()
@@ -456,6 +471,7 @@ def als_train(config: AlsConfig, a: RatingsMatrix, probe=None):
 
 class Algorithm(Enum):
     kAls = "als"
+    kCcd = "ccd"
     kCcdpp = "ccdpp"
 
 
@@ -478,6 +494,9 @@ def run_training(spec: RunSpec, a: RatingsMatrix, probe=None):
     if spec.algorithm == Algorithm.kCcdpp:
         return ccdpp_train(CcdConfig(spec.k, spec.lam, spec.outer_iters, spec.inner_iters, spec.workers, spec.seed),
                            a, probe)
+    if spec.algorithm == Algorithm.kCcd:
+        return ccd_train(CcdConfig(spec.k, spec.lam, spec.outer_iters, spec.inner_iters, spec.workers, spec.seed),
+                         a, probe)
     raise ValueError("unknown algorithm")
 
 
@@ -694,6 +713,18 @@ class Context:
     def ccdpp_iterate(self, n: int = 1) -> np.ndarray:
         secs = np.zeros(n)
         _check(lib.pmf_ctx_ccdpp_iterate(self.h, n, _ptr(secs)))
+        return secs
+
+    def ccd_begin(self, config: CcdConfig):
+        """Item/user-wise CCD (ccd.hpp:52-125) on the resident matrix."""
+        config.validate()
+        cfg = config._c()
+        _check(lib.pmf_ctx_ccd_begin(self.h, C.byref(cfg)))
+        self.k = config.k
+
+    def ccd_iterate(self, n: int = 1) -> np.ndarray:
+        secs = np.zeros(n)
+        _check(lib.pmf_ctx_ccd_iterate(self.h, n, _ptr(secs)))
         return secs
 
     def als_begin(self, config: AlsConfig):

@@ -1,0 +1,199 @@
+// ccdw_kernels.cu -- item/user-wise CCD (ccd.hpp:52-125, ccd_train :310-344) on the GPU.
+//
+// One CCD epoch updates every coordinate w_it (rows in order, t = 0..k-1 within a row) with the
+// closed-form 1-D minimiser z* = sum_j (R_ij + w_it h_jt) h_jt / (lambda + sum_j h_jt^2), shifting the
+// row's residual by (z* - w_it) h_jt, then mirrors the same for every h_jt over the columns.  Rows
+// only touch their own residual entries and W row while H is fixed, so the W sweep is exact with a
+// warp per row (the reference runs it on one worker only because it loops rows sequentially); the
+// same holds for columns in the H sweep, with a CTA per column (columns reach m entries).  Within a
+// row / column the t loop stays sequential.  The residual lives in CSR order for the W sweep and in
+// CSC order for the H sweep; between the sweeps one layout is copied into the other through the
+// position maps, so both stay bitwise equal (the reference's set_from_row / set_from_col mirror,
+// sparse.hpp:241-250).  Per-entry arithmetic rounds like the reference (products before adds); the
+// sums over a row / column are warp / CTA trees (reduction order differs, as everywhere on the GPU).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "device.hpp"
+
+namespace pmfgpu {
+
+namespace {
+
+constexpr int kRowCache = 8;      // residual entries per lane kept in registers (rows <= 256)
+constexpr int kColThreads = 256;
+
+// position maps between the two layouts: csr2csc[p] = q and csc2csr[q] = p
+__global__ void ccd_xlink_kernel(const int64_t* __restrict__ row_start, const int32_t* __restrict__ col_of,
+                                 const int64_t* __restrict__ col_start, const int32_t* __restrict__ row_of,
+                                 int32_t m, int32_t* __restrict__ csr2csc, int32_t* __restrict__ csc2csr) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < m;
+         i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        for (int64_t p = row_start[i] + lane; p < row_start[i + 1]; p += 32) {
+            const int32_t j = col_of[p];
+            int64_t lo = col_start[j], hi = col_start[j + 1];
+            while (lo < hi) {  // first position of column j whose row is >= i
+                const int64_t mid = (lo + hi) >> 1;
+                if (row_of[mid] < i) lo = mid + 1;
+                else hi = mid;
+            }
+            csr2csc[p] = static_cast<int32_t>(lo);
+            csc2csr[lo] = static_cast<int32_t>(p);
+        }
+    }
+}
+
+__global__ void ccd_gather_kernel(float* __restrict__ dst, const float* __restrict__ src,
+                                  const int32_t* __restrict__ map, int64_t n) {
+    for (int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; x < n;
+         x += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        dst[x] = src[map[x]];
+}
+
+__device__ __forceinline__ void warp_sum2(float& a, float& b) {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+        a += __shfl_xor_sync(0xffffffffu, a, off);
+        b += __shfl_xor_sync(0xffffffffu, b, off);
+    }
+}
+
+// W sweep (ccd.hpp:113-116): a warp per row; for each t the z* of ccd_z_star (:56-68) and the
+// residual shift of ccd_apply_z (:73-80).  The row's residual sits in registers for rows <= 256.
+__global__ void ccd_rows_kernel(const int64_t* __restrict__ row_start, const int32_t* __restrict__ col_of,
+                                float* __restrict__ R, float* __restrict__ W, const float* __restrict__ H,
+                                int32_t m, int k, float lambda) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < m;
+         i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const int64_t b = row_start[i], e = row_start[i + 1];
+        const bool cached = e - b <= 32 * kRowCache;
+        float r[kRowCache];
+        int32_t jj[kRowCache];
+        if (cached) {
+#pragma unroll
+            for (int c = 0; c < kRowCache; ++c) {
+                const int64_t p = b + lane + 32 * c;
+                r[c] = p < e ? R[p] : 0.f;
+                jj[c] = p < e ? col_of[p] : 0;
+            }
+        }
+        for (int t = 0; t < k; ++t) {
+            const float wit = W[i * k + t];
+            float num = 0.f, den = 0.f;
+            float hc[kRowCache];
+            if (cached) {
+#pragma unroll
+                for (int c = 0; c < kRowCache; ++c) {
+                    const bool in = b + lane + 32 * c < e;
+                    hc[c] = in ? H[static_cast<int64_t>(jj[c]) * k + t] : 0.f;
+                    if (in) {
+                        num = __fadd_rn(num, __fmul_rn(__fadd_rn(r[c], __fmul_rn(wit, hc[c])), hc[c]));
+                        den = __fadd_rn(den, __fmul_rn(hc[c], hc[c]));
+                    }
+                }
+            } else {
+                for (int64_t p = b + lane; p < e; p += 32) {
+                    const float h = H[static_cast<int64_t>(col_of[p]) * k + t];
+                    num = __fadd_rn(num, __fmul_rn(__fadd_rn(R[p], __fmul_rn(wit, h)), h));
+                    den = __fadd_rn(den, __fmul_rn(h, h));
+                }
+            }
+            warp_sum2(num, den);
+            const float dt = __fadd_rn(lambda, den);
+            const float z = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+            const float delta = __fsub_rn(z, wit);
+            if (cached) {
+#pragma unroll
+                for (int c = 0; c < kRowCache; ++c) r[c] = __fsub_rn(r[c], __fmul_rn(delta, hc[c]));
+            } else {
+                for (int64_t p = b + lane; p < e; p += 32)
+                    R[p] = __fsub_rn(R[p], __fmul_rn(delta, H[static_cast<int64_t>(col_of[p]) * k + t]));
+            }
+            if (lane == 0) W[i * k + t] = z;
+        }
+        if (cached) {
+#pragma unroll
+            for (int c = 0; c < kRowCache; ++c) {
+                const int64_t p = b + lane + 32 * c;
+                if (p < e) R[p] = r[c];
+            }
+        }
+    }
+}
+
+// H sweep (ccd.hpp:117-119): a CTA per column, ccd_s_star (:84-96) / ccd_apply_s (:99-106).
+__global__ void __launch_bounds__(kColThreads)
+ccd_cols_kernel(const int64_t* __restrict__ col_start, const int32_t* __restrict__ row_of, float* __restrict__ R,
+                const float* __restrict__ W, float* __restrict__ H, int32_t n, int k, float lambda) {
+    __shared__ float s_num[kColThreads / 32], s_den[kColThreads / 32];
+    __shared__ float s_z;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int64_t j = blockIdx.x; j < n; j += gridDim.x) {
+        const int64_t b = col_start[j], e = col_start[j + 1];
+        for (int t = 0; t < k; ++t) {
+            const float hjt = H[j * k + t];
+            float num = 0.f, den = 0.f;
+            for (int64_t q = b + threadIdx.x; q < e; q += kColThreads) {
+                const float w = W[static_cast<int64_t>(row_of[q]) * k + t];
+                num = __fadd_rn(num, __fmul_rn(__fadd_rn(R[q], __fmul_rn(w, hjt)), w));
+                den = __fadd_rn(den, __fmul_rn(w, w));
+            }
+            warp_sum2(num, den);
+            if (lane == 0) {
+                s_num[warp] = num;
+                s_den[warp] = den;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                num = lane < kColThreads / 32 ? s_num[lane] : 0.f;
+                den = lane < kColThreads / 32 ? s_den[lane] : 0.f;
+                warp_sum2(num, den);
+                if (lane == 0) {
+                    const float dt = __fadd_rn(lambda, den);
+                    s_z = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+                }
+            }
+            __syncthreads();
+            const float z = s_z;
+            const float delta = __fsub_rn(z, hjt);
+            for (int64_t q = b + threadIdx.x; q < e; q += kColThreads)
+                R[q] = __fsub_rn(R[q], __fmul_rn(delta, W[static_cast<int64_t>(row_of[q]) * k + t]));
+            if (threadIdx.x == 0) H[j * k + t] = z;
+            __syncthreads();  // H[j,t] and s_z settled before the next t
+        }
+    }
+}
+
+}  // namespace
+
+void launch_ccd_xlinks(const int64_t* row_start, const int32_t* col_of, const int64_t* col_start,
+                       const int32_t* row_of, int32_t m, int32_t* csr2csc, int32_t* csc2csr, cudaStream_t s) {
+    if (m <= 0) return;
+    ccd_xlink_kernel<<<148 * 8, 256, 0, s>>>(row_start, col_of, col_start, row_of, m, csr2csc, csc2csr);
+}
+
+int launch_ccd_epoch(const CcdWs& ws, float* W, float* H, int k, float lambda, cudaStream_t s) {
+    int launched = 0;
+    if (ws.m > 0) {
+        ccd_rows_kernel<<<148 * 8, 256, 0, s>>>(ws.row_start, ws.col_of, ws.R_row, W, H, ws.m, k, lambda);
+        ++launched;
+    }
+    if (ws.nnz > 0) {
+        ccd_gather_kernel<<<148 * 16, 256, 0, s>>>(ws.R_col, ws.R_row, ws.csc2csr, ws.nnz);  // set_from_row
+        ++launched;
+    }
+    if (ws.n > 0) {
+        ccd_cols_kernel<<<148 * 8, kColThreads, 0, s>>>(ws.col_start, ws.row_of, ws.R_col, W, H, ws.n, k, lambda);
+        ++launched;
+    }
+    if (ws.nnz > 0) {
+        ccd_gather_kernel<<<148 * 16, 256, 0, s>>>(ws.R_row, ws.R_col, ws.csr2csc, ws.nnz);  // set_from_col
+        ++launched;
+    }
+    return launched;
+}
+
+}  // namespace pmfgpu

@@ -102,6 +102,24 @@ cudaError_t ingest_build(const DevTriplet* t, int64_t nnz, int32_t m, int32_t n,
 void launch_probe_sse(const DevTriplet* probe, int64_t n, FactorView W, FactorView H, int k,
                       double* scratch, double* out, cudaStream_t stream);
 
+// ---- item/user-wise CCD (ccd.hpp:52-125), ccdw_kernels.cu -------------------------------------
+struct CcdWs {
+    int32_t m = 0, n = 0;
+    int64_t nnz = 0;
+    const int64_t* row_start = nullptr;
+    const int32_t* col_of = nullptr;
+    const int64_t* col_start = nullptr;
+    const int32_t* row_of = nullptr;
+    float* R_row = nullptr;      // residual, CSR order
+    float* R_col = nullptr;      // residual, CSC order
+    int32_t* csr2csc = nullptr;  // position maps (the reference's xlinks)
+    int32_t* csc2csr = nullptr;
+};
+void launch_ccd_xlinks(const int64_t* row_start, const int32_t* col_of, const int64_t* col_start,
+                       const int32_t* row_of, int32_t m, int32_t* csr2csc, int32_t* csc2csr, cudaStream_t s);
+// One epoch (W sweep, mirror, H sweep, mirror) on row-major W (m x k) / H (n x k).  Returns launches.
+int launch_ccd_epoch(const CcdWs& ws, float* W, float* H, int k, float lambda, cudaStream_t s);
+
 // ---- top_n (model.hpp:172-209), topn_kernels.cu ------------------------------------------------
 // For each of n_users users (W rows users[u]): the `count` best unrated items of W H^T (row-major
 // m x k, n x k), excluding ex_items[ex_start[u] .. ex_start[u+1]) (ascending).  out_* are

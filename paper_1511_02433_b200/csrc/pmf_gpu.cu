@@ -257,6 +257,9 @@ struct Ctx {
     // ALS
     bool als_built = false;
     DevMem als_mem;
+    DevMem ccdw_mem;   // item/user-wise CCD workspace
+    CcdWs ccdw;
+    bool ccdw_on = false;
     DevAls als_csr, als_csc;
     int* d_counter = nullptr;
     int* d_status = nullptr;
@@ -746,6 +749,7 @@ void als_begin(Ctx& c, const pmf_als_config* cfg) {
     c.k = cfg->k;
     c.lambda = cfg->lambda;
     c.als_weighted = (cfg->flags & PMF_ALS_WEIGHTED_LAMBDA) != 0;
+    c.ccdw_on = false;
     c.W = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_m + 1) * c.k);
     c.H = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_n + 1) * c.k);
     als_alloc_partials(c, c.k);
@@ -767,7 +771,7 @@ int64_t enqueue_als_iteration(Ctx& c) {
 }
 
 void als_iterate(Ctx& c, int n_outer, double* secs) {
-    if (c.mode != 2) invalid("als_begin has not been called");
+    if (c.mode != 2 || c.ccdw_on) invalid("als_begin has not been called");
     CUDA_TRY(cudaSetDevice(c.device));
     cudaEvent_t e0, e1;
     CUDA_TRY(cudaEventCreate(&e0));
@@ -784,6 +788,70 @@ void als_iterate(Ctx& c, int n_outer, double* secs) {
         int st = 0;
         CUDA_TRY(cudaMemcpy(&st, c.d_status, sizeof(int), cudaMemcpyDeviceToHost));
         if (st == 4) throw PmfError(PMF_NOT_POSITIVE_DEFINITE, "non-positive pivot in an ALS row solve");
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    CUDA_TRY(cudaGetLastError());
+}
+
+// ---- item/user-wise CCD (ccd.hpp:52-125, :310-344) ---------------------------------------------
+
+void ccdw_begin(Ctx& c, const pmf_ccd_config* cfg) {
+    if (!cfg) invalid("config is null");
+    if (cfg->k < 1) invalid("k must be >= 1");  // ccd.hpp:43-49
+    if (cfg->lambda < 0.f) invalid("lambda must be >= 0");
+    if (cfg->outer_iters < 1) invalid("outer_iters must be >= 1");
+    if (cfg->inner_iters < 1) invalid("inner_iters must be >= 1");
+    if (c.world != 1) invalid("item/user-wise CCD runs on one device (ccd.hpp:306-309)");
+    if (!c.als_built) invalid("context was created without the plain CSR / CSC layouts");
+    if (c.nnz >= (int64_t(1) << 31)) invalid("item/user-wise CCD: more than 2^31 - 1 ratings");
+    CUDA_TRY(cudaSetDevice(c.device));
+    reset_graph(c);
+    c.model_mem.free_all();
+    c.ccdw_mem.free_all();
+    c.k = cfg->k;
+    c.lambda = cfg->lambda;
+    CcdWs& w = c.ccdw;
+    w.m = c.m;
+    w.n = c.n;
+    w.nnz = c.nnz;
+    w.row_start = c.ccdw_mem.upload(c.row_start_local, c.stream, &c.h2d);
+    w.col_start = c.ccdw_mem.upload(c.col_start_local, c.stream, &c.h2d);
+    w.col_of = c.als_csr.idx;  // world == 1: the padded index space is the identity
+    w.row_of = c.als_csc.idx;
+    const size_t N = static_cast<size_t>(std::max<int64_t>(c.nnz, 1));
+    w.R_row = c.ccdw_mem.alloc<float>(N, false);
+    w.R_col = c.ccdw_mem.alloc<float>(N, false);
+    w.csr2csc = c.ccdw_mem.alloc<int32_t>(N, false);
+    w.csc2csr = c.ccdw_mem.alloc<int32_t>(N, false);
+    if (c.nnz > 0) {  // residual_from (sparse.hpp:259-262): R = A, W = 0
+        CUDA_TRY(cudaMemcpyAsync(w.R_row, c.als_csr.val, sizeof(float) * c.nnz, cudaMemcpyDeviceToDevice, c.stream));
+        CUDA_TRY(cudaMemcpyAsync(w.R_col, c.als_csc.val, sizeof(float) * c.nnz, cudaMemcpyDeviceToDevice, c.stream));
+    }
+    launch_ccd_xlinks(w.row_start, w.col_of, w.col_start, w.row_of, w.m, w.csr2csc, w.csc2csr, c.stream);
+    c.W = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_m + 1) * c.k);
+    c.H = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_n + 1) * c.k);
+    const auto H = init_items_host(c.n, cfg->k, cfg->seed);  // model.hpp:86-93
+    upload_rowmajor(c, c.H, c.ext_n, H.data(), c.n, cfg->k, false);
+    CUDA_TRY(cudaGetLastError());
+    c.mode = 2;  // row-major model: the ALS views serve metrics / model download
+    c.ccdw_on = true;
+}
+
+void ccdw_iterate(Ctx& c, int n_outer, double* secs) {
+    if (c.mode != 2 || !c.ccdw_on) invalid("ccd_begin has not been called");
+    CUDA_TRY(cudaSetDevice(c.device));
+    cudaEvent_t e0, e1;
+    CUDA_TRY(cudaEventCreate(&e0));
+    CUDA_TRY(cudaEventCreate(&e1));
+    for (int it = 0; it < n_outer; ++it) {
+        CUDA_TRY(cudaEventRecord(e0, c.stream));
+        c.launches_per_iter = launch_ccd_epoch(c.ccdw, c.W, c.H, c.k, c.lambda, c.stream);
+        CUDA_TRY(cudaEventRecord(e1, c.stream));
+        CUDA_TRY(cudaEventSynchronize(e1));
+        float ms = 0;
+        CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+        if (secs) secs[it] = ms * 1e-3;
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -1002,6 +1070,12 @@ pmf_status pmf_ctx_ccdpp_begin(pmf_ctx* ctx, const pmf_ccd_config* cfg) {
 }
 pmf_status pmf_ctx_ccdpp_iterate(pmf_ctx* ctx, int32_t n_outer, double* secs) {
     return guard([&] { ccd_iterate(*as_ctx(ctx), n_outer, secs); });
+}
+pmf_status pmf_ctx_ccd_begin(pmf_ctx* ctx, const pmf_ccd_config* cfg) {
+    return guard([&] { ccdw_begin(*as_ctx(ctx), cfg); });
+}
+pmf_status pmf_ctx_ccd_iterate(pmf_ctx* ctx, int32_t n_outer, double* secs) {
+    return guard([&] { ccdw_iterate(*as_ctx(ctx), n_outer, secs); });
 }
 pmf_status pmf_ctx_als_begin(pmf_ctx* ctx, const pmf_als_config* cfg) {
     return guard([&] { als_begin(*as_ctx(ctx), cfg); });
@@ -1328,6 +1402,21 @@ pmf_status pmf_ccdpp_train(const pmf_ccd_config* cfg, const pmf_matrix_view* a, 
     return train_common(
         a, cfg->outer_iters, probe, n_probe, W_out, H_out, rows, totals, [&](Ctx& c) { ccd_begin(c, cfg); },
         [&](Ctx& c, double* s) { ccd_iterate(c, 1, s); });
+}
+
+pmf_status pmf_ccd_train(const pmf_ccd_config* cfg, const pmf_matrix_view* a, const pmf_triplet* probe,
+                         int64_t n_probe, float* W_out, float* H_out, pmf_iter_row* rows, pmf_train_totals* totals) {
+    if (!cfg) {
+        g_err = "config is null";
+        return PMF_INVALID_ARGUMENT;
+    }
+    return train_common(
+        a, cfg->outer_iters, probe, n_probe, W_out, H_out, rows, totals,
+        [&](Ctx& c) {
+            build_als(c, a);
+            ccdw_begin(c, cfg);
+        },
+        [&](Ctx& c, double* s) { ccdw_iterate(c, 1, s); });
 }
 
 pmf_status pmf_als_train(const pmf_als_config* cfg, const pmf_matrix_view* a, const pmf_triplet* probe,

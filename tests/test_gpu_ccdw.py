@@ -1,0 +1,58 @@
+"""GPU item/user-wise CCD (ccd.hpp:52-125, ccd_train :310-344) against the oracle
+(pinned to the reference in test_ccd_oracle.py): per-iteration objective, train and probe RMSE within
+1e-4 relative, factors within 1e-3 relative Frobenius (sums over a row / column are warp / CTA trees,
+the reference's are sequential), objective non-increasing, edge cases."""
+import numpy as np
+import pytest
+
+from conftest import frob_rel, rel
+
+pytestmark = pytest.mark.gpu
+
+
+def test_ccd_ml100k_vs_oracle(pmf, oracle, ml100k):
+    train, probe = ml100k
+    A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
+    O = oracle.from_triplets(train, 943, 1682)
+    cfg = pmf.CcdConfig(k=10, lam=0.05, outer_iters=4, inner_iters=15, seed=1)
+    model, rep = pmf.ccd_train(cfg, A, probe)
+    W, H, rows = oracle.ccd_train(O, 10, 0.05, 4, 1, probe)
+    for r, g in zip(rep.rows, rows):
+        assert rel(r.objective, g["objective"]) < 1e-4
+        assert rel(r.rmse, g["rmse"]) < 1e-4
+        assert rel(r.train_rmse, g["train_rmse"]) < 1e-4
+    assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+    objs = [r.objective for r in rep.rows]
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(objs, objs[1:]))
+    assert pmf.run_training(pmf.RunSpec(pmf.Algorithm.kCcd, k=10, lam=0.05, outer_iters=4, inner_iters=15,
+                                        workers=1, seed=1), A, probe)[0] == model
+
+
+def test_ccd_edges_vs_oracle(pmf, oracle):
+    # empty rows / columns, lambda = 0 (den == 0 -> 0), a row longer than the register cache
+    t = oracle.random_triplets(57, 41, 300, 9)
+    t = np.concatenate([t, np.array([(60, j, 3.0) for j in range(41)] +
+                                    [(i, 44, 2.0) for i in range(0, 70, 2)], dtype=t.dtype)])
+    A = pmf.RatingsMatrix.from_triplets(t, 70, 45)
+    O = oracle.from_triplets(t, 70, 45)
+    for lam in (0.0, 0.2):
+        model, rep = pmf.ccd_train(pmf.CcdConfig(k=3, lam=lam, outer_iters=3, inner_iters=1, seed=5), A)
+        W, H, rows = oracle.ccd_train(O, 3, lam, 3, 5)
+        for r, g in zip(rep.rows, rows):
+            assert rel(r.objective, g["objective"]) < 1e-4
+        assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+    with pytest.raises(ValueError):
+        pmf.ccd_train(pmf.CcdConfig(k=0), A)
+
+
+@pytest.mark.slow
+def test_ccd_long_rows_vs_oracle(pmf, oracle):
+    m, n = 300, 5000
+    t = oracle.synth_ratings(m, n, 3, 400000, 3)   # rows of ~1300 entries: the uncached path
+    A = pmf.RatingsMatrix.from_triplets(t, m, n)
+    O = oracle.from_triplets(t, m, n)
+    model, rep = pmf.ccd_train(pmf.CcdConfig(k=5, lam=0.05, outer_iters=2, inner_iters=1, seed=2), A)
+    W, H, rows = oracle.ccd_train(O, 5, 0.05, 2, 2)
+    for r, g in zip(rep.rows, rows):
+        assert rel(r.objective, g["objective"]) < 1e-4
+    assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
