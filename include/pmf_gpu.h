@@ -218,6 +218,11 @@ pmf_status pmf_top_n(const float* W, const float* H, int32_t m, int32_t n, int32
                      const int32_t* users, int32_t n_users, int32_t count, const int64_t* ex_start,
                      const int32_t* ex_items, int32_t* out_items, float* out_scores, int32_t* out_count);
 
+/* ---- model files (model.hpp:211-295 save_model / load_model, the PMFB v1 format, float) ------
+ * load_model with W = H = NULL reads the header only; errors map to PMF_DATA_ERROR (data_error). */
+pmf_status pmf_save_model(const char* path, const float* W, const float* H, int64_t m, int64_t n, int64_t k);
+pmf_status pmf_load_model(const char* path, int64_t* m, int64_t* n, int64_t* k, float* W, float* H);
+
 /* ---- host helpers --------------------------------------------------------------------------- */
 
 /* runtime.hpp:91-136 partition_balanced (bounds has p+1 entries). */

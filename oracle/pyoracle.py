@@ -320,6 +320,8 @@ class Reference:
             getattr(L, "ref_als_sample" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, U64, P]
             getattr(L, "ref_top_n" + sfx).argtypes = [P, P, I32, I32, C.c_int, I32, I32, P, I64, P, P, P]
             getattr(L, "ref_ccd_train" + sfx).argtypes = [P, C.c_int, R, C.c_int, U64, P, I64, P, P, P]
+        L.ref_save_model_f32.argtypes = [C.c_char_p, P, P, I32, I32, C.c_int]
+        L.ref_load_model_f32.argtypes = [C.c_char_p, P, P, P]
         L.ref_synth_ratings.argtypes = [I32, I32, C.c_int, I64, U32, P]
         L.ref_synth_ratings.restype = I64
         L.ref_random_triplets.argtypes = [I32, I32, C.c_int, U32, F64, F64, P]
@@ -339,6 +341,17 @@ class Reference:
             if rc == 6:
                 raise ZeroDivisionError(msg)
             raise ValueError(msg)
+
+    def save_model(self, path, W, H):
+        W = np.ascontiguousarray(W, np.float32); H = np.ascontiguousarray(H, np.float32)
+        self._check(self.lib.ref_save_model_f32(os.fsencode(path), ptr(W), ptr(H), W.shape[0], H.shape[0], W.shape[1]))
+
+    def load_model(self, path):
+        mnk = np.zeros(3, np.int64)
+        self._check(self.lib.ref_load_model_f32(os.fsencode(path), ptr(mnk), None, None))
+        W = np.zeros((mnk[0], mnk[2]), np.float32); H = np.zeros((mnk[1], mnk[2]), np.float32)
+        self._check(self.lib.ref_load_model_f32(os.fsencode(path), ptr(mnk), ptr(W), ptr(H)))
+        return W, H
 
     def matrix(self, trips, m, n, real="_f32"):
         return RefMatrix(self, trips, m, n, real)

@@ -411,4 +411,24 @@ int ref_partition_balanced(const int64_t* costs, int32_t count, int p, int32_t* 
     })
 }
 
+// model.hpp:233-295 through the reference (float): files written by one side read by the other
+int ref_save_model_f32(const char* path, const float* W, const float* H, int32_t m, int32_t n, int k) {
+    GUARD({
+        FactorModel<float> model(m, n, k);
+        std::copy(W, W + model.w().size(), model.w().begin());
+        std::copy(H, H + model.h().size(), model.h().begin());
+        save_model(path, model);
+    })
+}
+int ref_load_model_f32(const char* path, int64_t* mnk, float* W, float* H) {
+    GUARD({
+        const auto model = load_model<float>(path);
+        mnk[0] = model.users();
+        mnk[1] = model.items();
+        mnk[2] = model.rank();
+        if (W) std::ranges::copy(model.w(), W);
+        if (H) std::ranges::copy(model.h(), H);
+    })
+}
+
 }  // extern "C"

@@ -44,7 +44,7 @@ __all__ = [
     "predict", "init_random_items", "ccdpp_build_rhat", "ccdpp_update_u", "ccdpp_update_v", "ccdpp_writeback",
     "solve_user_rows", "solve_item_rows", "cholesky_solve_batched", "partition_balanced", "synth_ratings",
     "Context", "DataError", "NotPositiveDefinite", "DomainError", "device_count", "nccl_unique_id", "dist_plan",
-    "top_n", "top_n_batch", "ccd_train",
+    "top_n", "top_n_batch", "ccd_train", "save_model", "load_model",
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -134,6 +134,8 @@ _SIGS = {
     "pmf_partition_balanced": ([_P, C.c_int32, C.c_int32, _P], C.c_int),
     "pmf_matrix_from_triplets": ([_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
     "pmf_matrix_from_triplets_gpu": ([_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pmf_save_model": ([C.c_char_p, _P, _P, C.c_int64, C.c_int64, C.c_int64], C.c_int),
+    "pmf_load_model": ([C.c_char_p, _P, _P, _P, _P, _P], C.c_int),
     "pmf_top_n": ([_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P], C.c_int),
     "pmf_synth_ratings": ([C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_uint32, _P, _P, _P, _P],
                           C.c_int),
@@ -285,6 +287,21 @@ class FactorModel:
 
     def __eq__(self, o):
         return isinstance(o, FactorModel) and np.array_equal(self.w, o.w) and np.array_equal(self.h, o.h)
+
+
+def save_model(path, model: "FactorModel"):
+    """model.hpp:233-248 save_model: the reference's PMFB v1 file (float), bit-exact round trip."""
+    W = np.ascontiguousarray(model.w, np.float32); H = np.ascontiguousarray(model.h, np.float32)
+    _check(lib.pmf_save_model(os.fsencode(path), _ptr(W), _ptr(H), W.shape[0], H.shape[0], W.shape[1]))
+
+
+def load_model(path) -> "FactorModel":
+    """model.hpp:270-295 load_model<float>; DataError like the reference's data_error."""
+    m, n, k = C.c_int64(), C.c_int64(), C.c_int64()
+    _check(lib.pmf_load_model(os.fsencode(path), C.byref(m), C.byref(n), C.byref(k), None, None))
+    W = np.empty((m.value, k.value), np.float32); H = np.empty((n.value, k.value), np.float32)
+    _check(lib.pmf_load_model(os.fsencode(path), C.byref(m), C.byref(n), C.byref(k), _ptr(W), _ptr(H)))
+    return FactorModel(W, H)
 
 
 def init_random_items(n: int, k: int, seed: int) -> np.ndarray:

@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <random>
@@ -334,3 +335,64 @@ pmf_status pmf_synth_ratings(int32_t m, int32_t n, int32_t true_rank, int64_t n_
 }
 
 }  // extern "C"
+
+// ---- model.hpp:211-295 PMFB model files (single precision) --------------------------------------
+// "PMFB", u32 version 1, u32 scalar size, i64 m, i64 n, i64 k, W (m*k), H (n*k), little-endian raw.
+pmf_status pmf_save_model(const char* path, const float* W, const float* H, int64_t m, int64_t n, int64_t k) {
+    if (!path || m < 0 || n < 0 || k < 1 || (m * k > 0 && !W) || (n * k > 0 && !H)) {
+        pmfgpu::set_error("save_model: invalid arguments");
+        return PMF_INVALID_ARGUMENT;
+    }
+    FILE* f = std::fopen(path, "wb");
+    if (!f) {
+        pmfgpu::set_error(std::string("cannot open ") + path + " for writing");
+        return PMF_DATA_ERROR;
+    }
+    const uint32_t version = 1, scalar = sizeof(float);
+    bool ok = std::fwrite("PMFB", 1, 4, f) == 4 && std::fwrite(&version, 4, 1, f) == 1 &&
+              std::fwrite(&scalar, 4, 1, f) == 1 && std::fwrite(&m, 8, 1, f) == 1 && std::fwrite(&n, 8, 1, f) == 1 &&
+              std::fwrite(&k, 8, 1, f) == 1;
+    ok = ok && (m * k == 0 || std::fwrite(W, sizeof(float), static_cast<size_t>(m * k), f) == static_cast<size_t>(m * k));
+    ok = ok && (n * k == 0 || std::fwrite(H, sizeof(float), static_cast<size_t>(n * k), f) == static_cast<size_t>(n * k));
+    ok = std::fclose(f) == 0 && ok;
+    if (!ok) {
+        pmfgpu::set_error(std::string("short write to ") + path);
+        return PMF_DATA_ERROR;
+    }
+    return PMF_OK;
+}
+
+// Reads the header (W, H == nullptr) or the whole model into caller buffers of the header's size.
+pmf_status pmf_load_model(const char* path, int64_t* m, int64_t* n, int64_t* k, float* W, float* H) {
+    if (!path || !m || !n || !k) {
+        pmfgpu::set_error("load_model: invalid arguments");
+        return PMF_INVALID_ARGUMENT;
+    }
+    FILE* f = std::fopen(path, "rb");
+    if (!f) {
+        pmfgpu::set_error(std::string("cannot open model file ") + path);
+        return PMF_DATA_ERROR;
+    }
+    auto fail = [&](const std::string& msg) {
+        std::fclose(f);
+        pmfgpu::set_error(msg);
+        return PMF_DATA_ERROR;
+    };
+    char magic[4];
+    uint32_t version = 0, scalar = 0;
+    if (std::fread(magic, 1, 4, f) != 4 || std::memcmp(magic, "PMFB", 4) != 0)
+        return fail(std::string(path) + " is not a model file");
+    if (std::fread(&version, 4, 1, f) != 1 || std::fread(&scalar, 4, 1, f) != 1 || version != 1)
+        return fail("unsupported model format version");
+    if (scalar != sizeof(float)) return fail("model precision does not match requested precision");
+    if (std::fread(m, 8, 1, f) != 1 || std::fread(n, 8, 1, f) != 1 || std::fread(k, 8, 1, f) != 1)
+        return fail("model file truncated: " + std::string(path));
+    if (*m < 0 || *n < 0 || *k < 1) return fail("corrupt model header");
+    if (W || H) {
+        const size_t wn = static_cast<size_t>(*m * *k), hn = static_cast<size_t>(*n * *k);
+        if ((wn && std::fread(W, sizeof(float), wn, f) != wn) || (hn && std::fread(H, sizeof(float), hn, f) != hn))
+            return fail("model file truncated: " + std::string(path));
+    }
+    std::fclose(f);
+    return PMF_OK;
+}
