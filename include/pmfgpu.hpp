@@ -101,6 +101,26 @@ inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> ccdpp_train(
                                                 config.outer_iters, config.inner_iters, config.seed, a, rows, tot)};
 }
 
+// ccd.hpp:310-344 (item/user-wise CCD; one device, inner_iters ignored like the reference)
+inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> ccd_train(
+    const parmf::CcdConfig<float>& config, const parmf::RatingsMatrix<float>& a,
+    parmf::span_arg<const parmf::Triplet<float>> probe) {
+    config.validate();
+    const pmf_ccd_config c{config.k, config.lambda, config.outer_iters, config.inner_iters, config.seed, 1, 0};
+    const pmf_matrix_view v = view_of(a);
+    parmf::FactorModel<float> model(a.rows(), a.cols(), config.k);
+    std::vector<pmf_iter_row> rows(static_cast<size_t>(config.outer_iters));
+    pmf_train_totals tot{};
+    check(pmf_ccd_train(&c, &v, probe_ptr(probe), static_cast<int64_t>(probe.size()), model.w().data(),
+                        model.h().data(), rows.data(), &tot));
+    if (probe.empty())
+        for (auto& r : rows) r.rmse = std::numeric_limits<double>::quiet_NaN();
+    auto rep = detail::report_of("ccd", config.k, static_cast<double>(config.lambda), config.outer_iters, 1,
+                                 config.seed, a, rows, tot);
+    rep.workers = 1;
+    return {std::move(model), std::move(rep)};
+}
+
 // als.hpp:188-233
 inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> als_train(
     const parmf::AlsConfig<float>& config, const parmf::RatingsMatrix<float>& a,
@@ -117,7 +137,7 @@ inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> als_train(
                                                 config.outer_iters, 1, config.seed, a, rows, tot)};
 }
 
-// bench.hpp:44-74 (float only; item/user-wise CCD has no GPU path and is rejected)
+// bench.hpp:44-74 (float only)
 inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> run_training(
     const parmf::RunSpec& spec, const parmf::RatingsMatrix<float>& a,
     parmf::span_arg<const parmf::Triplet<float>> probe) {
@@ -130,17 +150,46 @@ inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> run_training(
         c.seed = spec.seed;
         return als_train(c, a, probe);
     }
-    if (spec.algorithm == parmf::Algorithm::kCcdpp) {
-        parmf::CcdConfig<float> c;
-        c.k = spec.k;
-        c.lambda = static_cast<float>(spec.lambda);
-        c.outer_iters = spec.outer_iters;
-        c.inner_iters = spec.inner_iters;
-        c.workers = spec.workers;
-        c.seed = spec.seed;
-        return ccdpp_train(c, a, probe);
+    parmf::CcdConfig<float> c;
+    c.k = spec.k;
+    c.lambda = static_cast<float>(spec.lambda);
+    c.outer_iters = spec.outer_iters;
+    c.inner_iters = spec.inner_iters;
+    c.workers = spec.workers;
+    c.seed = spec.seed;
+    if (spec.algorithm == parmf::Algorithm::kCcd) {
+        c.variant = parmf::CcdVariant::kCcd;
+        return ccd_train(c, a, probe);
     }
-    throw std::invalid_argument("the B200 backend implements ccdpp and als");
+    return ccdpp_train(c, a, probe);
+}
+
+// model.hpp:172-198 top_n(model, i, count, rated_sorted), scored on the B200
+inline std::vector<std::pair<parmf::index_t, float>> top_n(const parmf::FactorModel<float>& model,
+                                                           parmf::index_t i, parmf::index_t count,
+                                                           std::span<const parmf::index_t> rated_sorted) {
+    const int32_t user = i;
+    const int64_t ex_start[2] = {0, static_cast<int64_t>(rated_sorted.size())};
+    const int32_t none = 0;
+    const size_t c = static_cast<size_t>(count > 0 ? count : 1);
+    std::vector<int32_t> items(c);
+    std::vector<float> scores(c);
+    int32_t got = 0;
+    check(pmf_top_n(model.w().data(), model.h().data(), model.users(), model.items(), model.rank(), &user, 1, count,
+                    ex_start, rated_sorted.empty() ? &none : rated_sorted.data(), items.data(), scores.data(), &got));
+    std::vector<std::pair<parmf::index_t, float>> out(static_cast<size_t>(got));
+    for (int32_t x = 0; x < got; ++x) out[static_cast<size_t>(x)] = {items[static_cast<size_t>(x)], scores[static_cast<size_t>(x)]};
+    return out;
+}
+
+// model.hpp:203-209 (rated items from the matrix row)
+inline std::vector<std::pair<parmf::index_t, float>> top_n(const parmf::FactorModel<float>& model,
+                                                           const parmf::RatingsMatrix<float>& a, parmf::index_t i,
+                                                           parmf::index_t count) {
+    std::vector<parmf::index_t> rated;
+    rated.reserve(static_cast<size_t>(a.row_nnz(i)));
+    for (const auto [item, pos] : a.row_slice(i)) rated.push_back(item);
+    return top_n(model, i, count, rated);
 }
 
 // model.hpp:156-167

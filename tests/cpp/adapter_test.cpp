@@ -36,6 +36,23 @@ int main() {
         std::printf("als iter %d objective ref %.10g gpu %.10g\n", ra.rows[i].iteration, ra.rows[i].objective, rg.rows[i].objective);
         bad += !close(rg.rows[i].objective, ra.rows[i].objective, 1e-4);
     }
+    // item/user-wise CCD through run_training's kCcd dispatch (ccd.hpp:310-344)
+    parmf::RunSpec spec;
+    spec.algorithm = parmf::Algorithm::kCcd;
+    spec.k = 10; spec.lambda = 0.05; spec.outer_iters = 2; spec.seed = 1;
+    const auto [mc_ref, rc_ref] = parmf::run_training(spec, a, std::span<const parmf::Triplet<float>>(probe));
+    const auto [mc_gpu, rc_gpu] = pmfgpu::run_training(spec, a, probe);
+    for (size_t i = 0; i < rc_ref.rows.size(); ++i) {
+        std::printf("ccd iter %d objective ref %.10g gpu %.10g\n", rc_ref.rows[i].iteration, rc_ref.rows[i].objective,
+                    rc_gpu.rows[i].objective);
+        bad += !close(rc_gpu.rows[i].objective, rc_ref.rows[i].objective, 1e-4);
+    }
+    // top_n: identical rankings and scores on the same model (model.hpp:172-209)
+    for (parmf::index_t i : {0, 17, 942}) {
+        const auto r1 = parmf::top_n(m_gpu, a, i, 25);
+        const auto r2 = pmfgpu::top_n(m_gpu, a, i, 25);
+        bad += r1 != r2;
+    }
     try {
         parmf::AlsConfig<float> badc;
         badc.lambda = 0.0f;
