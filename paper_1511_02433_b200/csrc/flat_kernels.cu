@@ -170,7 +170,7 @@ template <int FM, bool CSR>
 __device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[8], const FlatChunk& ch,
                                            const ChunkInfo& ci, int vb, float& cn, float& cd, int& ucur,
                                            float* __restrict__ R, float2* __restrict__ partial,
-                                           const SweepOperands& op, const float* g0) {
+                                           const SweepOperands& op, const float* g0, int sent) {
     constexpr bool kReduce = FM == kFPlain || FM == kFBuildSweep;
     constexpr bool kWrite = FM != kFPlain;
     const int lane = threadIdx.x & 31;
@@ -191,34 +191,35 @@ __device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[
     const uint32_t b2 = __ballot_sync(0xffffffffu, nib & 4u), b3 = __ballot_sync(0xffffffffu, nib & 8u);
     int uj = ucur + __popc(b0 & lt) + __popc(b1 & lt) + __popc(b2 & lt) + __popc(b3 & lt);
     const int ul = uj;
+    // branch-free over the lane's 4 vectors: entries of vectors outside the chunk read the zero
+    // sentinel slot with a zero residual (they add exactly 0 and are never stored)
     float pn[4], pd[4];
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
         pn[j] = pd[j] = 0.f;
+        const bool vj = (vmask >> j) & 1u;
         float fj = 0.f;
         if (kWrite) fj = __shfl_sync(0xffffffffu, fac, uj & 31);
-        if ((vmask >> j) & 1u) {
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int e = 4 * j + c;
-                const uint32_t w = ix[e >> 1];
-                const int gi = (e & 1) ? static_cast<int>(w >> 16) : static_cast<int>(w & 0xffffu);
-                const float g = g0[gi];
-                float rr = r[e];
-                if (FM == kFDemote) {
-                    rr = __fsub_rn(rr, __fmul_rn(fj, g));
-                } else if (FM == kFBuild || FM == kFBuildSweep) {
-                    // CSR: w = output factor, h = gathered; CSC: w = gathered, h = output factor
-                    const float wv = CSR ? fj : g;
-                    const float hv = CSR ? g : fj;
-                    if (wv != 0.f) rr = __fadd_rn(rr, __fmul_rn(wv, hv));
-                }
-                if (kReduce) {
-                    pn[j] = fmaf(rr, g, pn[j]);
-                    pd[j] = fmaf(g, g, pd[j]);
-                }
-                r[e] = rr;
+        for (int c = 0; c < 4; ++c) {
+            const int e = 4 * j + c;
+            const uint32_t w = ix[e >> 1];
+            const int gi = vj ? ((e & 1) ? static_cast<int>(w >> 16) : static_cast<int>(w & 0xffffu)) : sent;
+            const float g = g0[gi];
+            float rr = vj ? r[e] : 0.f;
+            if (FM == kFDemote) {
+                rr = __fsub_rn(rr, __fmul_rn(fj, g));
+            } else if (FM == kFBuild || FM == kFBuildSweep) {
+                // CSR: w = output factor, h = gathered; CSC: w = gathered, h = output factor
+                const float wv = CSR ? fj : g;
+                const float hv = CSR ? g : fj;
+                if (wv != 0.f) rr = __fadd_rn(rr, __fmul_rn(wv, hv));
             }
+            if (kReduce) {
+                pn[j] = fmaf(rr, g, pn[j]);
+                pd[j] = fmaf(g, g, pd[j]);
+            }
+            r[e] = rr;
         }
         uj += (nib >> j) & 1u;
     }
@@ -273,10 +274,12 @@ __device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[
         }
         // walk the lane's vectors from the open sum before it, emitting at every unit end
         int u = ul;
+        const uint32_t bj[4] = {b0, b1, b2, b3};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
             en += pn[j];
             ed += pd[j];
+            if (!bj[j]) continue;  // warp-uniform: no unit ends at this vector slot
             const int inf = __shfl_sync(0xffffffffu, info, u & 31);
             if ((nib >> j) & 1u) {
                 if (inf >= 0) {
@@ -310,14 +313,15 @@ __device__ __forceinline__ void load_block(float (&r)[16], uint32_t (&ix)[8], co
 template <int FM, bool CSR>
 __device__ __forceinline__ void flat_chunk(const FlatChunk& ch, const ChunkInfo& ci,
                                            const uint16_t* __restrict__ idx, float* __restrict__ R,
-                                           float2* __restrict__ partial, const SweepOperands& op, const float* g0) {
+                                           float2* __restrict__ partial, const SweepOperands& op, const float* g0,
+                                           int sent) {
     float cn = 0.f, cd = 0.f;
     int ucur = 0;
     for (int vb = ch.v0 & ~3; vb < ch.v1; vb += 128) {
         float r[16];
         uint32_t ix[8];
         load_block(r, ix, ch, vb, idx, R);
-        flat_block<FM, CSR>(r, ix, ch, ci, vb, cn, cd, ucur, R, partial, op, g0);
+        flat_block<FM, CSR>(r, ix, ch, ci, vb, cn, cd, ucur, R, partial, op, g0, sent);
     }
 }
 
@@ -450,7 +454,7 @@ flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, co
                 const bool same = nvb < ch1.v1;
                 if (same) load_block(rn, ixn, ch1, nvb, idx, R);
                 else if (c2 < cend) load_block(rn, ixn, ch2, ch2.v0 & ~3, idx, R);
-                flat_block<FM, CSR>(r, ix, ch1, ci1, vb, cn, cd, ucur, R, partial, op, smem);
+                flat_block<FM, CSR>(r, ix, ch1, ci1, vb, cn, cd, ucur, R, partial, op, smem, panel_size);
                 if (same) {
                     vb = nvb;
                 } else {
@@ -487,7 +491,7 @@ flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, co
                 const ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
                 const int c3 = cl.next();
                 const FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
-                flat_chunk<FM, CSR>(ch1, ci1, idx, R, partial, op, smem);
+                flat_chunk<FM, CSR>(ch1, ci1, idx, R, partial, op, smem, panel_size);
                 c1 = c2;
                 ch1 = ch2;
                 ci1 = ci2;
