@@ -141,9 +141,9 @@ __device__ __forceinline__ void st8(float* p, const float* r) {
 // fields are kept as they are and only combined where they are used (in flat_block), so a warp does
 // not stall on the descriptor loads of the chunk after next while it streams the current one.
 struct ChunkInfo {
-    int slot;       // the unit's partial slot, or < 0 for a direct write of output o
-    int o;
-    float fac;      // residual passes: the unit's output factor
+    int slotA, oA;  // unit ua + lane: partial slot (< 0: direct write of output o)
+    int slotB, oB;  // unit ua + 32 + lane
+    float facA, facB;  // residual passes: the units' output factors
     uint32_t tw;    // tail word w0 + lane
 };
 
@@ -152,14 +152,21 @@ __device__ __forceinline__ ChunkInfo chunk_info(const FlatChunk& ch, const Unit*
                                                 const uint32_t* __restrict__ tb, const SweepOperands& op) {
     constexpr bool kWrite = FM != kFPlain;
     const int lane = threadIdx.x & 31;
-    ChunkInfo ci{0, 0, 0.f, 0u};
-    const int ui = min(ch.ua + lane, max(ch.ub - 1, 0));  // clamped: every lane loads (no branch)
-    const int2 so = *reinterpret_cast<const int2*>(&units[ui].o);
-    ci.o = so.x;
-    ci.slot = so.y;
-    if (kWrite) ci.fac = (FM == kFDemote ? op.oa : op.ob)[op.out_off + so.x];
+    ChunkInfo ci{0, 0, 0, 0, 0.f, 0.f, 0u};
+    const int last = max(ch.ub - 1, 0);
+    const int2 a = *reinterpret_cast<const int2*>(&units[min(ch.ua + lane, last)].o);  // clamped: no branch
+    const int2 b = *reinterpret_cast<const int2*>(&units[min(ch.ua + 32 + lane, last)].o);
+    ci.oA = a.x;
+    ci.slotA = a.y;
+    ci.oB = b.x;
+    ci.slotB = b.y;
+    if (kWrite) {
+        const float* f = FM == kFDemote ? op.oa : op.ob;
+        ci.facA = f[op.out_off + a.x];
+        ci.facB = f[op.out_off + b.x];
+    }
     const int w0 = ch.v0 >> 5;
-    ci.tw = __ldg(tb + w0 + min(lane, 9));
+    ci.tw = __ldg(tb + w0 + min(lane, kFlatChunkVectors / 32 + 1));
     return ci;
 }
 
@@ -176,8 +183,8 @@ __device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int v0 = ch.v0, v1 = ch.v1;
-    const int info = ci.slot >= 0 ? ci.slot : -(ci.o + 1);  // slot, or -(output + 1): direct write
-    const float fac = ci.fac;
+    // slot, or -(output + 1): direct write
+    const int infoA = ci.slotA >= 0 ? ci.slotA : -(ci.oA + 1), infoB = ci.slotB >= 0 ? ci.slotB : -(ci.oB + 1);
     const int w0 = v0 >> 5;
     const uint32_t tw = ci.tw;
     const int lv = vb + 4 * lane;
@@ -199,7 +206,10 @@ __device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[
         pn[j] = pd[j] = 0.f;
         const bool vj = (vmask >> j) & 1u;
         float fj = 0.f;
-        if (kWrite) fj = __shfl_sync(0xffffffffu, fac, uj & 31);
+        if (kWrite) {
+            const float fa = __shfl_sync(0xffffffffu, ci.facA, uj & 31), fb = __shfl_sync(0xffffffffu, ci.facB, uj & 31);
+            fj = uj < 32 ? fa : fb;
+        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             const int e = 4 * j + c;
@@ -280,7 +290,8 @@ __device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[
             en += pn[j];
             ed += pd[j];
             if (!bj[j]) continue;  // warp-uniform: no unit ends at this vector slot
-            const int inf = __shfl_sync(0xffffffffu, info, u & 31);
+            const int ia = __shfl_sync(0xffffffffu, infoA, u & 31), ib = __shfl_sync(0xffffffffu, infoB, u & 31);
+            const int inf = u < 32 ? ia : ib;
             if ((nib >> j) & 1u) {
                 if (inf >= 0) {
                     partial[inf] = make_float2(en, ed);

@@ -468,7 +468,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
 
     if (L.flat) {
         if (L.n_entries / 4 >= (int64_t(1) << 31)) throw std::length_error("too many vectors for a flat layout");
-        L.tailbits.assign(static_cast<size_t>(L.n_entries / 4 / 32 + 12), 0u);  // slack: chunk prologues load 10 words
+        L.tailbits.assign(static_cast<size_t>(L.n_entries / 4 / 32 + 24), 0u);  // slack: chunk prologues load 18 words
         for (const Unit& u : L.units) {
             const int64_t last = (static_cast<int64_t>(u.e0) + u.len) / 4 - 1;
             L.tailbits[last >> 5] |= 1u << (last & 31);

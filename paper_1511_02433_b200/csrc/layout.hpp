@@ -85,8 +85,8 @@ struct Piece {
 struct FlatChunk {
     int32_t ua, v0, v1, ub;
 };
-constexpr int kFlatChunkVectors = 256;
-constexpr int kFlatChunkUnits = 32;  // a warp holds a chunk's unit descriptors in one register per lane
+constexpr int kFlatChunkVectors = 512;
+constexpr int kFlatChunkUnits = 64;  // a warp holds a chunk's unit descriptors in two registers per lane
 
 struct SweepLayout {
     int32_t n_out = 0;        // outputs on this side (local)
@@ -126,7 +126,7 @@ struct SweepLayout {
     // whole units; tailbits marks the last 4-entry vector of every unit.
     bool flat = false;
     std::vector<FlatChunk> chunks;    // pieces' chunks: Piece::pad[0..1] = chunk range
-    std::vector<uint32_t> tailbits;   // (n_entries / 4) bits + 12 words of slack
+    std::vector<uint32_t> tailbits;   // (n_entries / 4) bits + 24 words of slack
 };
 
 // Shared-memory floats one staged vector of `width` occupies (sentinel slot, 16-byte rounded).
