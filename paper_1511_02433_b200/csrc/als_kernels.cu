@@ -197,6 +197,120 @@ __device__ __forceinline__ bool warp_cholesky_solve_exact(float* G, float& b0, f
     return true;
 }
 
+// warp_cholesky_solve for the tensor-core kernels' gram (row stride GS: 16-byte rows, GS / 4 odd):
+// the lane's row and the pivot row are read 4 columns at a time with 128-bit loads (the pivot row is a
+// broadcast, the lanes' rows are conflict-free), and the second row set of a lane (i0 + 32) is only
+// visited while it exists (j < k - 33, warp-uniform).  Sums are formed in the same order as
+// warp_cholesky_solve, so the factor is bitwise the same.
+template <int KMAX, int GS>
+__device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
+    static_assert(GS % 4 == 0 && (GS / 4) % 2 == 1, "row stride must be an odd multiple of 4 floats");
+    const int lane = threadIdx.x & 31;
+    bool ok = true;
+    for (int j = 0; j < k; ++j) {
+        const int i0 = j + 1 + lane, i1 = i0 + 32;
+        const bool h0 = i0 < k;
+        const float* Gj = G + j * GS;
+        const float* G0 = G + (h0 ? i0 : j) * GS;
+        float d0 = Gj[j], d1 = 0.f, d2 = 0.f, d3 = 0.f;
+        float s0 = h0 ? G0[j] : 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+        int t = 0;
+        if (KMAX > 32 && j < k - 33) {  // some lanes own a second row i1
+            const bool h1 = i1 < k;
+            const float* G1 = G + (h1 ? i1 : j) * GS;
+            float r0 = h1 ? G1[j] : 0.f, r1 = 0.f;
+            for (; t + 4 <= j; t += 4) {
+                const float4 g = *reinterpret_cast<const float4*>(Gj + t);
+                const float4 a = *reinterpret_cast<const float4*>(G0 + t);
+                const float4 c = *reinterpret_cast<const float4*>(G1 + t);
+                d0 = fmaf(-g.x, g.x, d0);
+                d1 = fmaf(-g.y, g.y, d1);
+                d2 = fmaf(-g.z, g.z, d2);
+                d3 = fmaf(-g.w, g.w, d3);
+                s0 = fmaf(-a.x, g.x, s0);
+                s1 = fmaf(-a.y, g.y, s1);
+                s2 = fmaf(-a.z, g.z, s2);
+                s3 = fmaf(-a.w, g.w, s3);
+                r0 = fmaf(-c.x, g.x, r0);
+                r1 = fmaf(-c.y, g.y, r1);
+                r0 = fmaf(-c.z, g.z, r0);
+                r1 = fmaf(-c.w, g.w, r1);
+            }
+            for (; t < j; ++t) {
+                const float g0 = Gj[t];
+                d0 = fmaf(-g0, g0, d0);
+                s0 = fmaf(-G0[t], g0, s0);
+                r0 = fmaf(-G1[t], g0, r0);
+            }
+            const float d = (d0 + d1) + (d2 + d3);
+            if (!(d > 0.f)) {
+                ok = false;
+                break;
+            }
+            const float ljj = sqrtf(d);
+            const float rl = 1.0f / ljj;
+            __syncwarp();
+            if (h0) G[i0 * GS + j] = G[j * GS + i0] = ((s0 + s1) + (s2 + s3)) * rl;
+            if (h1) G[i1 * GS + j] = G[j * GS + i1] = (r0 + r1) * rl;
+            if (lane == 0) G[j * GS + j] = ljj;
+            __syncwarp();
+            continue;
+        }
+        for (; t + 4 <= j; t += 4) {
+            const float4 g = *reinterpret_cast<const float4*>(Gj + t);
+            const float4 a = *reinterpret_cast<const float4*>(G0 + t);
+            d0 = fmaf(-g.x, g.x, d0);
+            d1 = fmaf(-g.y, g.y, d1);
+            d2 = fmaf(-g.z, g.z, d2);
+            d3 = fmaf(-g.w, g.w, d3);
+            s0 = fmaf(-a.x, g.x, s0);
+            s1 = fmaf(-a.y, g.y, s1);
+            s2 = fmaf(-a.z, g.z, s2);
+            s3 = fmaf(-a.w, g.w, s3);
+        }
+        for (; t < j; ++t) {
+            const float g0 = Gj[t];
+            d0 = fmaf(-g0, g0, d0);
+            s0 = fmaf(-G0[t], g0, s0);
+        }
+        const float d = (d0 + d1) + (d2 + d3);
+        if (!(d > 0.f)) {
+            ok = false;
+            break;
+        }
+        const float ljj = sqrtf(d);
+        const float rl = 1.0f / ljj;
+        __syncwarp();
+        if (h0) G[i0 * GS + j] = G[j * GS + i0] = ((s0 + s1) + (s2 + s3)) * rl;
+        if (lane == 0) G[j * GS + j] = ljj;
+        __syncwarp();
+    }
+    if (!ok) return false;
+    // forward: L y = b (column-oriented; L^T mirrored in the upper triangle: row reads, no conflicts)
+    for (int i = 0; i < k; ++i) {
+        const float bi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
+        const float yi = bi / G[i * GS + i];
+        if (lane == (i & 31)) {
+            if (i < 32) b0 = yi;
+            else b1 = yi;
+        }
+        if (lane > i && lane < k) b0 = fmaf(-G[i * GS + lane], yi, b0);
+        if (KMAX > 32 && lane + 32 > i && lane + 32 < k) b1 = fmaf(-G[i * GS + lane + 32], yi, b1);
+    }
+    // backward: L^T x = y
+    for (int i = k - 1; i >= 0; --i) {
+        const float yi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
+        const float xi = yi / G[i * GS + i];
+        if (lane == (i & 31)) {
+            if (i < 32) b0 = xi;
+            else b1 = xi;
+        }
+        if (lane < i) b0 = fmaf(-G[i * GS + lane], xi, b0);
+        if (KMAX > 32 && lane + 32 < i) b1 = fmaf(-G[i * GS + lane + 32], xi, b1);
+    }
+    return true;
+}
+
 // Stages the gathered opposing rows of one 32-entry chunk into X[s][0..KS): lanes own features
 // (coalesced 4k-byte row reads), 8 rows' loads are issued before they are stored (bank-conflict
 // free stores); columns [k, KS) and rows [cnt, rows_pad) are zero.
@@ -330,7 +444,12 @@ struct TcGeo {
     static constexpr int KS = (NT % 2) ? 8 * NT : 8 * NT + 8;  // staged row stride (bank-conflict free)
     static constexpr int JN = NT > 2 * MT ? NT : 2 * MT;      // feature slots per lane: g + 8j
     static constexpr int STAGE = 32 * KS;
-    static constexpr int GRAM = KMAX * (KMAX + 1) + 2 * KMAX;
+    // gram row stride: a multiple of 4 (16-byte rows for 128-bit loads) that is an odd multiple of 4
+    // modulo 32, so the rows of 8 consecutive lanes fall in distinct 4-bank groups (conflict-free
+    // LDS.128 of the lanes' own rows in the Cholesky)
+    static constexpr int GS0 = (KMAX + 1 + 3) & ~3;
+    static constexpr int GS = (GS0 % 8 == 0) ? GS0 + 4 : GS0;
+    static constexpr int GRAM = KMAX * GS + 2 * KMAX;
     // staged rows and the gram are separate regions: the rows arrive by TMA bulk copies (async
     // proxy) and the padding columns of X stay zero for the kernel's lifetime
     static constexpr int WARP_FLOATS = STAGE + GRAM + 64;
@@ -367,7 +486,7 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
                    int* __restrict__ counter, int* __restrict__ status, int tma, int exact) {
     using T = TcGeo<NT, MT>;
     constexpr int KS = T::KS, JN = T::JN, NTILES = T::NTILES, KMAX = T::KMAX;
-    constexpr int GS = KMAX + 1;
+    constexpr int GS = T::GS;
     extern __shared__ float smem[];
     __shared__ __align__(8) uint64_t s_bar[kAlsWarps];
     const int lane = threadIdx.x & 31;
@@ -512,8 +631,9 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
             continue;
         }
         __syncwarp();
-        const bool ok = (exact && k == KMAX) ? warp_cholesky_solve_exact<KMAX, GS>(G, rhs0, rhs1)
-                                             : warp_cholesky_solve<KMAX>(G, k, rhs0, rhs1);
+        const bool ok = exact == 2 ? true  // timing experiment only (PMF_ALS_EXACT=2): no factorisation
+                        : (exact && k == KMAX) ? warp_cholesky_solve_exact<KMAX, GS>(G, rhs0, rhs1)
+                                               : warp_cholesky_solve_v4<KMAX, GS>(G, k, rhs0, rhs1);
         if (!ok) {
             if (lane == 0) atomicExch(status, 4);
             rhs0 = rhs1 = 0.f;
@@ -626,8 +746,8 @@ bool use_tensor_cores() {
     return tc;
 }
 
-bool als_exact_chol() {
-    static const bool on = std::getenv("PMF_ALS_EXACT") != nullptr && std::atoi(std::getenv("PMF_ALS_EXACT")) != 0;
+int als_exact_chol() {
+    static const int on = std::getenv("PMF_ALS_EXACT") != nullptr ? std::atoi(std::getenv("PMF_ALS_EXACT")) : 0;
     return on;
 }
 
@@ -643,7 +763,7 @@ void launch_tc(const DevAls& L, const float* opp, float* out, int32_t out_off, i
     const int tma = tma_on && k % 4 == 0 && (reinterpret_cast<uintptr_t>(opp) & 15) == 0 ? 1 : 0;
     als_gram_tc_kernel<NT, MT><<<blocks, kAlsThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off,
                                                                 k, lambda, weighted ? 1 : 0, L.partial, d_counter,
-                                                                d_status, tma, als_exact_chol() ? 1 : 0);
+                                                                d_status, tma, als_exact_chol());
 }
 
 template <int KMAX>
