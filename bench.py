@@ -200,6 +200,7 @@ def run_ours(args, rank, world, dist):
                 "vsweep": {"ms": st["vsweep_ms"], "launches": st["vsweep_launches"], "gbs": round(v_ach, 1)}}
     res["roofline"] = roof
     res["ctx"] = ctx
+    res["nccl_id"] = nccl_id
     res["A"], res["probe"], res["train"] = A, probe, train
     return res
 
@@ -294,21 +295,33 @@ def main():
         return
 
     res = run_ours(args, rank, world, dist)
+    e2e = None
+    if not args.no_e2e and not dist:
+        # the public API end to end (a fresh context per call, as a user would make it); measured with
+        # no other context alive
+        res["ctx"].close()
+        e2e = e2e_ours(args, res["A"], res["probe"])
     als = None
     if solver == "ccdpp" and not args.no_als and args.config == "netflix-ccdpp":
-        ctx = res["ctx"]
-        ctx.als_begin(__import__("paper_1511_02433_b200").AlsConfig(k=k, lam=lam, outer_iters=1, seed=MODEL_SEED))
+        import paper_1511_02433_b200 as P
+        device = int(os.environ.get("LOCAL_RANK", "0"))
+        ctx = res["ctx"] if res["ctx"].h else P.Context(res["A"], device=device, rank=rank, world=world,
+                                                        nccl_id=res.get("nccl_id"))
+        ctx.als_begin(P.AlsConfig(k=k, lam=lam, outer_iters=1, seed=MODEL_SEED))
         ctx.als_iterate(1)
         barrier(dist)
         ts = [max_over_ranks(dist, s) for s in ctx.als_iterate(max(1, args.steps))]
         o, r, t = ctx.metrics()
         als = {"metric": "sec/outer-iter ALS k=40 Netflix shape", "value": float(np.mean(ts)), "unit": unit,
                "launches_per_iter": ctx.launch_count(), "objective": o, "rmse": r}
+        ctx.close()
+    res["ctx"].close()
     ingest = None
     if rank == 0 and not dist:
         # RatingsMatrix::from_triplets on the GPU vs the host build (same bytes out)
         import paper_1511_02433_b200 as P
         tr = res["train"]
+        P.RatingsMatrix.from_triplets(tr[:100000], m, n, device=True)  # one-time module load / staging set-up
         t0 = time.perf_counter()
         Ag = P.RatingsMatrix.from_triplets(tr, m, n, device=True)
         t_gpu = time.perf_counter() - t0
@@ -320,10 +333,6 @@ def main():
         ingest = {"from_triplets_gpu_s": round(t_gpu, 3), "from_triplets_host_s": round(t_host, 3),
                   "host_threads": os.cpu_count(), "bitwise_equal": bool(same), "nnz": int(len(tr))}
         del Ag, Ah
-    e2e = None
-    if not args.no_e2e and not dist:
-        res["ctx"].close()
-        e2e = e2e_ours(args, res["A"], res["probe"])
     cpu = None
     if rank == 0 and not dist and not args.no_cpu_baseline and solver == "ccdpp":
         try:
