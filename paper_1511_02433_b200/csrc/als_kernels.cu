@@ -206,6 +206,7 @@ template <int KMAX, int GS>
 __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
     static_assert(GS % 4 == 0 && (GS / 4) % 2 == 1, "row stride must be an odd multiple of 4 floats");
     const int lane = threadIdx.x & 31;
+    float* Rinv = G + KMAX * GS;  // 1 / L_jj (the solves multiply instead of dividing)
     bool ok = true;
     for (int j = 0; j < k; ++j) {
         const int i0 = j + 1 + lane, i1 = i0 + 32;
@@ -252,7 +253,10 @@ __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
             __syncwarp();
             if (h0) G[i0 * GS + j] = G[j * GS + i0] = ((s0 + s1) + (s2 + s3)) * rl;
             if (h1) G[i1 * GS + j] = G[j * GS + i1] = (r0 + r1) * rl;
-            if (lane == 0) G[j * GS + j] = ljj;
+            if (lane == 0) {
+                G[j * GS + j] = ljj;
+                Rinv[j] = rl;
+            }
             __syncwarp();
             continue;
         }
@@ -282,14 +286,17 @@ __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
         const float rl = 1.0f / ljj;
         __syncwarp();
         if (h0) G[i0 * GS + j] = G[j * GS + i0] = ((s0 + s1) + (s2 + s3)) * rl;
-        if (lane == 0) G[j * GS + j] = ljj;
+        if (lane == 0) {
+            G[j * GS + j] = ljj;
+            Rinv[j] = rl;
+        }
         __syncwarp();
     }
     if (!ok) return false;
     // forward: L y = b (column-oriented; L^T mirrored in the upper triangle: row reads, no conflicts)
     for (int i = 0; i < k; ++i) {
         const float bi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
-        const float yi = bi / G[i * GS + i];
+        const float yi = bi * Rinv[i];
         if (lane == (i & 31)) {
             if (i < 32) b0 = yi;
             else b1 = yi;
@@ -300,7 +307,7 @@ __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
     // backward: L^T x = y
     for (int i = k - 1; i >= 0; --i) {
         const float yi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
-        const float xi = yi / G[i * GS + i];
+        const float xi = yi * Rinv[i];
         if (lane == (i & 31)) {
             if (i < 32) b0 = xi;
             else b1 = xi;
