@@ -250,6 +250,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-als", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="reference arm: skip the top_n / CCD timings")
     args = ap.parse_args()
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -285,12 +286,31 @@ def main():
             vals = [M.als_sample(k, lam, cores, 1, MODEL_SEED) for _ in range(args.steps)]
             sample = "one full ALS epoch (W then H phase) per step"
         v = float(np.mean(vals))
+        extra = None
+        if solver == "ccdpp" and args.config == "netflix-ccdpp" and not args.no_extra:
+            # the reference's other predict / solver paths the B200 build covers, timed
+            # here so DESIGN.md's comparisons are reproducible: top_n per user (model.hpp:172) on this
+            # matrix, and one item/user-wise CCD epoch (ccd.hpp:310, always one worker) at ML-10M shape
+            rng = np.random.default_rng(1)
+            Wm = rng.normal(0, 0.3, (m, k)).astype(np.float32); Hm = rng.normal(0, 0.3, (n, k)).astype(np.float32)
+            R = Reference()
+            t0 = time.perf_counter()
+            for i in range(100):
+                R.top_n(Wm, Hm, i, 10, A.col_of[A.row_start[i]:A.row_start[i + 1]])
+            topn_ms = (time.perf_counter() - t0) / 100 * 1e3
+            mm, nn, ntr2, *_ = CONFIGS["ml10m-als"]
+            tr10, _, _ = make_data("ml10m-als")
+            _, _, rows = R.matrix(tr10, mm, nn, "_f32").ccd_train(10, 0.05, 1, 1)
+            extra = {"top_n_ms_per_user_1thread": round(topn_ms, 2),
+                     "ccd_train_ml10m_k10_epoch_s_1worker": round(float(rows["seconds"][0]), 3)}
         line = {"impl": "reference", "metric": f"sec/outer-iter {solver} (lower is better)", "value": v, "unit": unit,
                 "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v * 1e3,
                 "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
                 "data": "synthetic", "config": workload,
                 "cpu_baseline": {"value": v, "unit": unit, "cores": cores, "kind": "reference", "sample": sample},
                 "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        if extra:
+            line["reference_extra"] = extra
         print(json.dumps(line), flush=True)
         return
 

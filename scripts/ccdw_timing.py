@@ -1,5 +1,5 @@
-"""Item/user-wise CCD epoch time at the Netflix shape (k=40) on the device, and the reference's
-ccd_train on the ML-10M shape (single worker, as the reference always runs it)."""
+"""Item/user-wise CCD epoch time at the Netflix (k=40) and ML-10M (k=10) shapes on the device.  The
+reference's ccd_train is timed by `bench.py --impl reference`."""
 import os
 import sys
 import time
@@ -18,9 +18,3 @@ for cfg in ("netflix-ccdpp", "ml10m-als"):
     secs = ctx.ccd_iterate(3)
     print(f"{cfg} k={k}: GPU CCD epoch s {list(secs)} metrics {ctx.metrics()}", file=sys.stderr)
     ctx.close()
-    if cfg.startswith("ml10m"):
-        from oracle.pyoracle import Reference
-        M = Reference().matrix(train, m, n, "_f32")
-        t0 = time.perf_counter()
-        W, H, rows = M.ccd_train(k, 0.05, 1, 1)
-        print(f"{cfg} reference ccd_train 1 epoch: {rows['seconds'][0]:.2f} s (1 worker)", file=sys.stderr)

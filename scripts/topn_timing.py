@@ -1,5 +1,5 @@
 """Wall time of top_n_batch (pmf_top_n, copies included) for every user of the Netflix-shape matrix
-(k=40, count=10, rated items excluded) next to the reference's top_n on a sample of users."""
+(k=40, count=10, rated items excluded).  The reference's top_n is timed by `bench.py --impl reference`."""
 import os
 import sys
 import time
@@ -20,15 +20,3 @@ for rep in range(2):
     t0 = time.perf_counter()
     items, scores, counts = P.top_n_batch(model, users, 10, a=A)
     print(f"top_n_batch all {A.m} users: {time.perf_counter() - t0:.3f} s", file=sys.stderr)
-try:
-    from oracle.pyoracle import Reference
-    R = Reference()
-    t0 = time.perf_counter()
-    for i in range(200):
-        rated = A.col_of[A.row_start[i]:A.row_start[i + 1]]
-        ref = R.top_n(model.w, model.h, i, 10, rated)
-        assert [j for j, _ in ref] == list(items[i, :10])
-    dt = time.perf_counter() - t0
-    print(f"reference top_n: {dt / 200 * 1e3:.2f} ms/user (1 thread) -> {dt / 200 * A.m:.1f} s for all users", file=sys.stderr)
-except Exception as e:
-    print("reference unavailable:", e, file=sys.stderr)
