@@ -223,6 +223,11 @@ pmf_status pmf_top_n(const float* W, const float* H, int32_t m, int32_t n, int32
 pmf_status pmf_save_model(const char* path, const float* W, const float* H, int64_t m, int64_t n, int64_t k);
 pmf_status pmf_load_model(const char* path, int64_t* m, int64_t* n, int64_t* k, float* W, float* H);
 
+/* io.hpp:240-285 split_dataset: to_probe[e] = 1 for the entries the reference moves to the probe set
+ * (users[] = the external user id of every rating, file order). */
+pmf_status pmf_split_mask(const int64_t* users, int64_t n, double ratio, uint64_t seed, uint8_t* to_probe,
+                          int64_t* n_probe);
+
 /* ---- host helpers --------------------------------------------------------------------------- */
 
 /* runtime.hpp:91-136 partition_balanced (bounds has p+1 entries). */

@@ -321,6 +321,7 @@ class Reference:
             getattr(L, "ref_top_n" + sfx).argtypes = [P, P, I32, I32, C.c_int, I32, I32, P, I64, P, P, P]
             getattr(L, "ref_ccd_train" + sfx).argtypes = [P, C.c_int, R, C.c_int, U64, P, I64, P, P, P]
         L.ref_save_model_f32.argtypes = [C.c_char_p, P, P, I32, I32, C.c_int]
+        L.ref_split.argtypes = [P, P, P, I64, F64, U64, P, P, P, P]
         L.ref_load_model_f32.argtypes = [C.c_char_p, P, P, P]
         L.ref_synth_ratings.argtypes = [I32, I32, C.c_int, I64, U32, P]
         L.ref_synth_ratings.restype = I64
@@ -341,6 +342,15 @@ class Reference:
             if rc == 6:
                 raise ZeroDivisionError(msg)
             raise ValueError(msg)
+
+    def split(self, users, items, ratings, ratio, seed):
+        """io.hpp:240-285 split_dataset: the probe rows (file order)."""
+        u = np.ascontiguousarray(users, np.int64); i = np.ascontiguousarray(items, np.int64)
+        r = np.ascontiguousarray(ratings, np.float64)
+        pu = np.zeros(max(len(u), 1), np.int64); pi = np.zeros(max(len(u), 1), np.int64)
+        pr = np.zeros(max(len(u), 1), np.float64); n = np.zeros(1, np.int64)
+        self._check(self.lib.ref_split(ptr(u), ptr(i), ptr(r), len(u), ratio, seed, ptr(pu), ptr(pi), ptr(pr), ptr(n)))
+        return pu[:n[0]], pi[:n[0]], pr[:n[0]]
 
     def save_model(self, path, W, H):
         W = np.ascontiguousarray(W, np.float32); H = np.ascontiguousarray(H, np.float32)

@@ -431,4 +431,20 @@ int ref_load_model_f32(const char* path, int64_t* mnk, float* W, float* H) {
     })
 }
 
+// io.hpp:240-285 split_dataset through the reference: the probe rows, in file order
+int ref_split(const int64_t* users, const int64_t* items, const double* ratings, int64_t n, double ratio,
+              uint64_t seed, int64_t* probe_users, int64_t* probe_items, double* probe_ratings, int64_t* n_probe) {
+    GUARD({
+        std::vector<RawTriplet> all(static_cast<size_t>(n));
+        for (int64_t e = 0; e < n; ++e) all[static_cast<size_t>(e)] = {users[e], items[e], ratings[e]};
+        const auto sp = split_dataset(all, ratio, seed);
+        for (size_t x = 0; x < sp.probe.size(); ++x) {
+            probe_users[x] = sp.probe[x].user;
+            probe_items[x] = sp.probe[x].item;
+            probe_ratings[x] = sp.probe[x].rating;
+        }
+        *n_probe = static_cast<int64_t>(sp.probe.size());
+    })
+}
+
 }  // extern "C"

@@ -134,6 +134,7 @@ _SIGS = {
     "pmf_partition_balanced": ([_P, C.c_int32, C.c_int32, _P], C.c_int),
     "pmf_matrix_from_triplets": ([_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
     "pmf_matrix_from_triplets_gpu": ([_P, C.c_int64, C.c_int32, C.c_int32, _P, _P, _P, _P, _P, _P], C.c_int),
+    "pmf_split_mask": ([_P, C.c_int64, C.c_double, C.c_uint64, _P, _P], C.c_int),
     "pmf_save_model": ([C.c_char_p, _P, _P, C.c_int64, C.c_int64, C.c_int64], C.c_int),
     "pmf_load_model": ([C.c_char_p, _P, _P, _P, _P, _P], C.c_int),
     "pmf_top_n": ([_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P], C.c_int),

@@ -12,6 +12,7 @@
 #include <random>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/pmf_gpu.h"
@@ -394,5 +395,44 @@ pmf_status pmf_load_model(const char* path, int64_t* m, int64_t* n, int64_t* k, 
             return fail("model file truncated: " + std::string(path));
     }
     std::fclose(f);
+    return PMF_OK;
+}
+
+// ---- io.hpp:240-285 split_dataset (the probe mask; deterministic per seed) ------------------------
+// Users with a single rating stay in train, no user loses their last training rating; `ratio` is the
+// probe fraction of the eligible entries, drawn by a Fisher-Yates shuffle with std::mt19937(seed)
+// and gen() % i exactly as the reference.
+pmf_status pmf_split_mask(const int64_t* users, int64_t n, double ratio, uint64_t seed, uint8_t* to_probe,
+                          int64_t* n_probe) {
+    if (!(ratio > 0.0 && ratio < 1.0)) {
+        pmfgpu::set_error("split ratio must be in (0, 1)");
+        return PMF_INVALID_ARGUMENT;
+    }
+    if (n < 0 || (n > 0 && (!users || !to_probe)) || !n_probe || n >= (int64_t(1) << 32)) {
+        pmfgpu::set_error("split: invalid arguments");
+        return PMF_INVALID_ARGUMENT;
+    }
+    std::unordered_map<int64_t, int64_t> per_user;
+    for (int64_t e = 0; e < n; ++e) per_user[users[e]]++;
+    std::vector<uint32_t> eligible;
+    eligible.reserve(static_cast<size_t>(n));
+    for (uint32_t e = 0; e < static_cast<uint32_t>(n); ++e)
+        if (per_user[users[e]] >= 2) eligible.push_back(e);
+    std::mt19937 gen(static_cast<std::mt19937::result_type>(seed));
+    for (uint32_t i = static_cast<uint32_t>(eligible.size()); i > 1; --i)
+        std::swap(eligible[i - 1], eligible[gen() % i]);
+    const auto target = static_cast<size_t>(std::llround(ratio * static_cast<double>(eligible.size())));
+    std::memset(to_probe, 0, static_cast<size_t>(n));
+    std::unordered_map<int64_t, int64_t> left = per_user;
+    size_t taken = 0;
+    for (const auto e : eligible) {
+        if (taken >= target) break;
+        auto& remaining = left[users[e]];
+        if (remaining <= 1) continue;
+        --remaining;
+        to_probe[e] = 1;
+        ++taken;
+    }
+    *n_probe = static_cast<int64_t>(taken);
     return PMF_OK;
 }
