@@ -8,6 +8,7 @@
 // (left-looking by column, the order of dense.hpp:74-96) and forward/back substitution; chunks of
 // long columns write (G, b) partials that a second kernel sums in chunk order before solving.
 // A non-positive pivot sets the status word to PMF_NOT_POSITIVE_DEFINITE (dense.hpp:82-84).
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -442,8 +443,8 @@ als_gram_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_t* 
 // ---- tensor-core gram (3xTF32) -----------------------------------------------------------------
 // G = X^T X over the unit's gathered rows X (entries x features) with mma.sync m16n8k8 TF32: the
 // feature axis is tiled 16 (M) x 8 (N), the entry axis is the MMA K.  Only tiles touching the upper
-// triangle are computed (9 of 15 at k = 40).  Each operand is split x = hi + lo (hi = tf32(x),
-// lo = tf32(x - hi)) and G accumulates hi*hi + hi*lo + lo*hi in FP32, which keeps ~FP32 accuracy
+// triangle are computed (9 of 15 at k = 40).  Each operand is split x = hi + lo (split_tf32) and G
+// accumulates hi*hi + hi*lo + lo*hi in FP32, which keeps ~FP32 accuracy
 // (the north_star's 3xTF32 condition; parity is checked against the reference in the tests).
 template <int NT, int MT>
 struct TcGeo {
@@ -459,7 +460,7 @@ struct TcGeo {
     static constexpr int GRAM = KMAX * GS + 2 * KMAX;
     // staged rows and the gram are separate regions: the rows arrive by TMA bulk copies (async
     // proxy) and the padding columns of X stay zero for the kernel's lifetime
-    static constexpr int WARP_FLOATS = STAGE + GRAM + 64;
+    static constexpr int WARP_FLOATS = (STAGE + GRAM + 64 + 31) & ~31;  // 128-byte aligned stages (TMA)
     static constexpr int count_tiles() {
         int c = 0;
         for (int mi = 0; mi < MT; ++mi)
@@ -470,15 +471,18 @@ struct TcGeo {
     static constexpr int NTILES = count_tiles();
 };
 
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
+// x = hi + lo for the 3xTF32 products: hi = x rounded to nearest (ties away) at the TF32 mantissa
+// width by integer add + mask (2 instructions; sm_100's cvt.rna.tf32 is a 4-instruction sequence
+// with an inf/NaN guard that finite factors do not need), lo = x - hi exactly in FP32, then
+// truncated to TF32 (the MMA reads only the top 19 bits).
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+    hi = (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+    lo = __float_as_uint(x - __uint_as_float(hi)) & 0xffffe000u;
 }
 
 __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                                          uint32_t b0, uint32_t b1) {
-    asm volatile(
+    asm(  // not volatile: the compiler may interleave independent accumulators
         "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
         "{%0,%1,%2,%3};"
         : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
@@ -490,11 +494,12 @@ __global__ void __launch_bounds__(kAlsThreads)
 als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_t* __restrict__ idx,
                    const float* __restrict__ val, const float* __restrict__ opp, float* __restrict__ out,
                    int32_t out_off, int k, float lambda, int weighted, float* __restrict__ partial,
-                   int* __restrict__ counter, int* __restrict__ status, int tma, int exact) {
+                   int* __restrict__ counter, int* __restrict__ status, int tma, int exact,
+                   const __grid_constant__ CUtensorMap rows_map) {
     using T = TcGeo<NT, MT>;
     constexpr int KS = T::KS, JN = T::JN, NTILES = T::NTILES, KMAX = T::KMAX;
     constexpr int GS = T::GS;
-    extern __shared__ float smem[];
+    extern __shared__ __align__(128) float smem[];
     __shared__ __align__(8) uint64_t s_bar[kAlsWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -525,12 +530,49 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
         float acc[NTILES][4];
 #pragma unroll
         for (int t = 0; t < NTILES; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+        float accr[MT][4];
+#pragma unroll
+        for (int t = 0; t < MT; ++t) accr[t][0] = accr[t][1] = accr[t][2] = accr[t][3] = 0.f;
         float rhs0 = 0.f, rhs1 = 0.f;
         for (int base = 0; base < U.len; base += 32) {
             const int cnt = min(32, U.len - base);
             const int cnt8 = (cnt + 7) & ~7;
             __syncwarp();
-            if (tma) {
+            if (tma == 2) {
+                // TMA gather4: one elected lane issues cnt8 / 4 tensor copies of 4 rows each (rows past
+                // cnt use an out-of-bounds row coordinate and arrive zero-filled); X's row stride is k
+                const int row = lane < cnt ? idx[U.e0 + base + lane] : 0x7fffffff;
+                if (lane < cnt) sval[lane] = val[U.e0 + base + lane];
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                const uint32_t b = static_cast<uint32_t>(__cvta_generic_to_shared(bar));
+                if (lane == 0)
+                    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b),
+                                 "r"(static_cast<uint32_t>(cnt8 * k * 4))
+                                 : "memory");
+                for (int q = 0; q < cnt8; q += 4) {
+                    const int r0 = __shfl_sync(0xffffffffu, row, q), r1 = __shfl_sync(0xffffffffu, row, q + 1);
+                    const int r2 = __shfl_sync(0xffffffffu, row, q + 2), r3 = __shfl_sync(0xffffffffu, row, q + 3);
+                    if (lane == 0)
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+                            " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(
+                                static_cast<uint32_t>(__cvta_generic_to_shared(X + q * KS))),
+                            "l"(reinterpret_cast<uint64_t>(&rows_map)), "r"(0), "r"(r0), "r"(r1), "r"(r2), "r"(r3),
+                            "r"(b)
+                            : "memory");
+                }
+                asm volatile(
+                    "{\n"
+                    ".reg .pred p;\n"
+                    "ALSG_%=:\n"
+                    "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+                    "@!p bra ALSG_%=;\n"
+                    "}\n" ::"r"(b),
+                    "r"(phase)
+                    : "memory");
+                phase ^= 1;
+            } else if (tma) {
                 // one bulk copy per gathered row, issued by the row's lane, completing on the warp's
                 // mbarrier; the rows past cnt up to the MMA's multiple of 8 are zeroed
                 const int row = lane < cnt ? idx[U.e0 + base + lane] : 0;
@@ -577,31 +619,50 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
 #pragma unroll
                     for (int h = 0; h < 2; ++h) {
                         const float x = j < NT ? X[(e0 + tig + 4 * h) * KS + 8 * j + g] : 0.f;
-                        hi[j][h] = to_tf32(x);
-                        lo[j][h] = to_tf32(x - __uint_as_float(hi[j][h]));
+                        split_tf32(x, hi[j][h], lo[j][h]);
                     }
-                int t = 0;
+                // the ratings as one more B column block (column 8 NT, lanes g == 0): X^T a rides the
+                // same MMAs as the gram instead of a per-entry FMA loop
+                uint32_t ahi[2], alo[2];
 #pragma unroll
-                for (int mi = 0; mi < MT; ++mi)
+                for (int h = 0; h < 2; ++h) {
+                    const int e = e0 + tig + 4 * h;
+                    const float av = (g == 0 && e < cnt) ? sval[e] : 0.f;
+                    split_tf32(av, ahi[h], alo[h]);
+                }
+                // three passes (hi*hi, hi*lo, lo*hi) over all tiles: consecutive MMAs are independent
 #pragma unroll
-                    for (int ni = 0; ni < NT; ++ni) {
-                        if (8 * ni + 7 < 16 * mi) continue;
-                        mma_tf32(acc[t], hi[2 * mi][0], hi[2 * mi + 1][0], hi[2 * mi][1], hi[2 * mi + 1][1],
-                                 hi[ni][0], hi[ni][1]);
-                        mma_tf32(acc[t], hi[2 * mi][0], hi[2 * mi + 1][0], hi[2 * mi][1], hi[2 * mi + 1][1],
-                                 lo[ni][0], lo[ni][1]);
-                        mma_tf32(acc[t], lo[2 * mi][0], lo[2 * mi + 1][0], lo[2 * mi][1], lo[2 * mi + 1][1],
-                                 hi[ni][0], hi[ni][1]);
-                        ++t;
+                for (int pass = 0; pass < 3; ++pass) {
+                    int t = 0;
+#pragma unroll
+                    for (int mi = 0; mi < MT; ++mi) {
+                        const uint32_t(&A)[JN][2] = pass == 2 ? lo : hi;
+#pragma unroll
+                        for (int ni = 0; ni < NT; ++ni) {
+                            if (8 * ni + 7 < 16 * mi) continue;
+                            const uint32_t(&B)[JN][2] = pass == 1 ? lo : hi;
+                            mma_tf32(acc[t], A[2 * mi][0], A[2 * mi + 1][0], A[2 * mi][1], A[2 * mi + 1][1],
+                                     B[ni][0], B[ni][1]);
+                            ++t;
+                        }
+                        mma_tf32(accr[mi], A[2 * mi][0], A[2 * mi + 1][0], A[2 * mi][1], A[2 * mi + 1][1],
+                                 pass == 1 ? alo[0] : ahi[0], pass == 1 ? alo[1] : ahi[1]);
                     }
-                const int ee = min(8, cnt - e0);
-                for (int e = 0; e < ee; ++e) {
-                    const float av = sval[e0 + e];
-                    const float* xs = X + (e0 + e) * KS;
-                    if (lane < k) rhs0 = fmaf(av, xs[lane], rhs0);
-                    if (lane + 32 < k) rhs1 = fmaf(av, xs[lane + 32], rhs1);
                 }
             }
+        }
+        // X^T a: lanes tig == 0 hold features 16 mi + g (+ 8) in accumulator elements 0 and 2
+        {
+            float* Bv = G + KMAX * GS + KMAX;  // past Rinv
+#pragma unroll
+            for (int mi = 0; mi < MT; ++mi)
+                if (tig == 0) {
+                    if (16 * mi + g < KMAX) Bv[16 * mi + g] = accr[mi][0];
+                    if (16 * mi + g + 8 < KMAX) Bv[16 * mi + g + 8] = accr[mi][2];
+                }
+            __syncwarp();
+            rhs0 = lane < k ? Bv[lane] : 0.f;
+            rhs1 = lane + 32 < k ? Bv[lane + 32] : 0.f;
         }
         __syncwarp();
         // scatter the upper-triangle tiles (and their mirror) into the gram / partial
@@ -758,23 +819,62 @@ int als_exact_chol() {
     return on;
 }
 
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_tiled() {
+    static const EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// 2-D tensor map over the opposing factor (n_opp rows of k floats) with a 1-row box of k floats:
+// the gather4 staging's descriptor (rows outside [0, n_opp) arrive zero-filled).
+bool make_rows_map(CUtensorMap* map, const float* opp, int64_t n_opp, int k) {
+    const EncodeTiledFn fn = encode_tiled();
+    if (!fn || n_opp <= 0) return false;
+    const cuuint64_t dims[2] = {static_cast<cuuint64_t>(k), static_cast<cuuint64_t>(n_opp)};
+    const cuuint64_t strides[1] = {static_cast<cuuint64_t>(k) * sizeof(float)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(k), 1u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    return fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(opp), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// PMF_ALS_TMA: unset = gather4 where the staged row stride equals k (else per-row bulk copies),
+// 1 = per-row bulk copies, 0 = LSU staging.
+int als_tma_mode() {
+    static const int m = std::getenv("PMF_ALS_TMA") ? std::atoi(std::getenv("PMF_ALS_TMA")) : 2;
+    return m;
+}
+
 template <int NT, int MT>
-void launch_tc(const DevAls& L, const float* opp, float* out, int32_t out_off, int k, float lambda, bool weighted,
-               int* d_counter, int* d_status, int sm_count, cudaStream_t s) {
+void launch_tc(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k, float lambda,
+               bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t s) {
     const size_t sm = smem_for_tc<NT, MT>();
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_gram_tc_kernel<NT, MT>, kAlsThreads, sm);
     const int blocks = std::max(1, std::min<int>(per_sm * sm_count, (L.n_units + kAlsWarps - 1) / kAlsWarps));
     // TMA row staging needs 16-byte rows (k % 4 == 0; the factor base is cudaMalloc-aligned)
-    static const bool tma_on = std::getenv("PMF_ALS_TMA") == nullptr || std::atoi(std::getenv("PMF_ALS_TMA")) != 0;
-    const int tma = tma_on && k % 4 == 0 && (reinterpret_cast<uintptr_t>(opp) & 15) == 0 ? 1 : 0;
+    const int mode = als_tma_mode();
+    int tma = mode != 0 && k % 4 == 0 && (reinterpret_cast<uintptr_t>(opp) & 15) == 0 ? 1 : 0;
+    alignas(64) CUtensorMap map{};
+    if (tma && mode == 2 && k == TcGeo<NT, MT>::KS && make_rows_map(&map, opp, n_opp, k)) tma = 2;
     als_gram_tc_kernel<NT, MT><<<blocks, kAlsThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off,
                                                                 k, lambda, weighted ? 1 : 0, L.partial, d_counter,
-                                                                d_status, tma, als_exact_chol());
+                                                                d_status, tma, als_exact_chol(), map);
 }
 
 template <int KMAX>
-int launch_k(const DevAls& L, const float* opp, float* out, int32_t out_off, int k, float lambda, bool weighted,
+int launch_k(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k, float lambda, bool weighted,
              int* d_counter, int* d_status, int sm_count, cudaStream_t s) {
     int launched = 0;
     const size_t sm = smem_for<KMAX>();
@@ -784,7 +884,7 @@ int launch_k(const DevAls& L, const float* opp, float* out, int32_t out_off, int
             // N tiles (8 features) and M tiles (16 features) covering the k features
             const int nt = (k + 7) / 8, mt = (k + 15) / 16;
 #define PMF_TC(NT_, MT_) \
-    if (nt == NT_ && mt == MT_) launch_tc<NT_, MT_>(L, opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, s)
+    if (nt == NT_ && mt == MT_) launch_tc<NT_, MT_>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, s)
             PMF_TC(1, 1); else PMF_TC(2, 1); else PMF_TC(3, 1); else PMF_TC(3, 2); else PMF_TC(4, 2);
             else PMF_TC(5, 2); else PMF_TC(5, 3); else PMF_TC(6, 3);
 #undef PMF_TC
@@ -846,13 +946,13 @@ void als_set_attributes() {
     set_attr_k<64>();
 }
 
-int launch_als_half(const DevAls& L, const float* opp, float* out, int32_t out_off, int k, float lambda,
-                    bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t stream) {
-    if (k <= 8) return launch_k<8>(L, opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
-    if (k <= 16) return launch_k<16>(L, opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
-    if (k <= 32) return launch_k<32>(L, opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
-    if (k <= 40) return launch_k<40>(L, opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
-    return launch_k<64>(L, opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
+int launch_als_half(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k,
+                    float lambda, bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t stream) {
+    if (k <= 8) return launch_k<8>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
+    if (k <= 16) return launch_k<16>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
+    if (k <= 32) return launch_k<32>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
+    if (k <= 40) return launch_k<40>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
+    return launch_k<64>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
 }
 
 void launch_cholesky_batched(float* a, float* x, int batch, int k, int* d_status, cudaStream_t s) {

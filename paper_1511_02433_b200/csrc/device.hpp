@@ -144,9 +144,9 @@ struct DevAls {
 };
 
 // Solves every output row of one side: out row (out_off + o) of the row-major factor `out`
-// (stride k) from the row-major opposing factor `opp`.  status: device int set to 4 on a
-// non-positive pivot.  Returns kernels launched.
-int launch_als_half(const DevAls& L, const float* opp, float* out, int32_t out_off, int k,
+// (stride k) from the row-major opposing factor `opp` (n_opp addressable rows).  status: device int
+// set to 4 on a non-positive pivot.  Returns kernels launched.
+int launch_als_half(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k,
                     float lambda, bool weighted, int* d_counter, int* d_status, int sm_count,
                     cudaStream_t stream);
 void als_set_attributes();

@@ -761,11 +761,11 @@ void als_begin(Ctx& c, const pmf_als_config* cfg) {
 int64_t enqueue_als_iteration(Ctx& c) {
     int64_t launched = 0;
     // W phase from the old H, then H phase from the new W (als.hpp:176-184)
-    launched += launch_als_half(c.als_csr, c.H, c.W, c.rank * c.Bm, c.k, c.lambda, c.als_weighted, c.d_counter,
-                                c.d_status, c.sm_count, c.stream);
+    launched += launch_als_half(c.als_csr, c.H, c.ext_n, c.W, c.rank * c.Bm, c.k, c.lambda, c.als_weighted,
+                                c.d_counter, c.d_status, c.sm_count, c.stream);
     allgather(c, c.W, static_cast<int64_t>(c.Bm) * c.k);
-    launched += launch_als_half(c.als_csc, c.W, c.H, c.rank * c.Bn, c.k, c.lambda, c.als_weighted, c.d_counter + 1,
-                                c.d_status, c.sm_count, c.stream);
+    launched += launch_als_half(c.als_csc, c.W, c.ext_m, c.H, c.rank * c.Bn, c.k, c.lambda, c.als_weighted,
+                                c.d_counter + 1, c.d_status, c.sm_count, c.stream);
     allgather(c, c.H, static_cast<int64_t>(c.Bn) * c.k);
     return launched;
 }
@@ -1580,8 +1580,8 @@ pmf_status pmf_als_solve_rows(const pmf_matrix_view* a, int32_t side, const floa
         als_alloc_partials(*c, k);
         CUDA_TRY(cudaMemcpy(opp, opposing, sizeof(float) * (side == 0 ? c->n : c->m) * k, cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemset(c->d_status, 0, sizeof(int)));
-        launch_als_half(side == 0 ? c->als_csr : c->als_csc, opp, dst, 0, k, lambda, false, c->d_counter, c->d_status,
-                        c->sm_count, c->stream);
+        launch_als_half(side == 0 ? c->als_csr : c->als_csc, opp, side == 0 ? c->n : c->m, dst, 0, k, lambda, false,
+                        c->d_counter, c->d_status, c->sm_count, c->stream);
         CUDA_TRY(cudaStreamSynchronize(c->stream));
         int st = 0;
         CUDA_TRY(cudaMemcpy(&st, c->d_status, sizeof(int), cudaMemcpyDeviceToHost));
