@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <future>
 #include <mutex>
 #include <thread>
 #include <memory>
@@ -430,8 +431,13 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     const double t_layout = now_s();
     c->hcsr = build_sweep_layout(a->row_start, a->col_of, a->val_row, c->row_begin, c->row_end, cmap, c->ext_n,
                                  2, smem_budget(), c->sm_count);
-    c->hcsc = build_sweep_layout(a->col_start, a->row_of, a->val_col, c->col_begin, c->col_end, rmap, c->ext_m,
-                                 3, smem_budget(), c->sm_count);
+    // the CSC layout is built on a host thread while the CSR layout uploads (the future's destructor
+    // waits for the builder if anything below throws)
+    static const bool serial = std::getenv("PMF_SETUP_SERIAL") != nullptr;
+    auto csc_future = std::async(serial ? std::launch::deferred : std::launch::async, [&] {
+        return build_sweep_layout(a->col_start, a->row_of, a->val_col, c->col_begin, c->col_end, rmap, c->ext_m, 3,
+                                  smem_budget(), c->sm_count);
+    });
     c->local_nnz_csr = a->row_start[c->row_end] - a->row_start[c->row_begin];
     c->local_nnz_csc = a->col_start[c->col_end] - a->col_start[c->col_begin];
     c->row_start_local.assign(a->row_start + c->row_begin, a->row_start + c->row_end + 1);
@@ -445,6 +451,9 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     }
     const double t_upload = now_s();
     c->csr = upload_sweep(*c, c->hcsr, &c->A_csr);
+    const double t_csr = now_s();
+    c->hcsc = csc_future.get();
+    const double t_csc = now_s();
     c->csc = upload_sweep(*c, c->hcsc, &c->A_csc);
     const double t_done = now_s();
     // eval scratch
@@ -454,8 +463,11 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     CUDA_TRY(cudaStreamSynchronize(c->stream));
     c->setup_seconds = now_s() - t0;
     if (std::getenv("PMF_VERBOSE"))
-        std::fprintf(stderr, "[pmf] ctx setup %.3f s: device init %.3f, layouts %.3f, upload %.3f, rest %.3f\n",
-                     c->setup_seconds, t_layout - t0, t_upload - t_layout, t_done - t_upload, now_s() - t_done);
+        std::fprintf(stderr,
+                     "[pmf] ctx setup %.3f s: device init %.3f, csr layout %.3f, csr upload %.3f (csc layout "
+                     "in parallel), csc wait %.3f, csc upload %.3f, rest %.3f\n",
+                     c->setup_seconds, t_layout - t0, t_upload - t_layout, t_csr - t_upload, t_csc - t_csr,
+                     t_done - t_csc, now_s() - t_done);
     return c;
 }
 
@@ -912,14 +924,19 @@ void get_model(Ctx& c, float* W, float* H) {
     const int k = c.k;
     if (c.mode == 1 && c.world == 1) {
         // transpose column-major k x ld -> row-major on the device, then a staged download
+        const double t0 = now_s();
         DevMem tmp;
         float* wt = tmp.alloc<float>(static_cast<size_t>(c.m) * k, false);
         float* ht = tmp.alloc<float>(static_cast<size_t>(c.n) * k, false);
         launch_transpose(c.W, c.ldm, k, c.m, wt, c.stream);
         launch_transpose(c.H, c.ldn, k, c.n, ht, c.stream);
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+        const double t1 = now_s();
         if (W) staged_d2h(W, wt, sizeof(float) * c.m * k, c.stream);
         if (H) staged_d2h(H, ht, sizeof(float) * c.n * k, c.stream);
         CUDA_TRY(cudaStreamSynchronize(c.stream));
+        if (std::getenv("PMF_VERBOSE"))
+            std::fprintf(stderr, "[pmf] get_model: alloc + transpose %.3f s, download %.3f s\n", t1 - t0, now_s() - t1);
         c.d2h += static_cast<int64_t>(sizeof(float) * (static_cast<int64_t>(c.m) + c.n) * k);
     } else if (c.mode == 1) {
         std::vector<float> w(static_cast<size_t>(k) * c.ldm), h(static_cast<size_t>(k) * c.ldn);
