@@ -41,7 +41,30 @@ __device__ double block_sum(double v, double* sm) {
     return r;
 }
 
-template <bool IDX16>
+// row-major factor rows with k % 4 == 0 are read as float4 (the products and their order are the
+// same either way: t ascending, each product rounded before the add)
+template <bool VEC>
+__device__ __forceinline__ double dot_double(FactorView W, int64_t i, FactorView H, int64_t j, int k) {
+    double pred = 0.0;
+    if (VEC) {
+        const float4* wr = reinterpret_cast<const float4*>(W.p + i * W.si);
+        const float4* hr = reinterpret_cast<const float4*>(H.p + j * H.si);
+        for (int t4 = 0; t4 < (k >> 2); ++t4) {
+            const float4 w = wr[t4], h = hr[t4];
+            pred = __dadd_rn(pred, __dmul_rn(static_cast<double>(w.x), static_cast<double>(h.x)));
+            pred = __dadd_rn(pred, __dmul_rn(static_cast<double>(w.y), static_cast<double>(h.y)));
+            pred = __dadd_rn(pred, __dmul_rn(static_cast<double>(w.z), static_cast<double>(h.z)));
+            pred = __dadd_rn(pred, __dmul_rn(static_cast<double>(w.w), static_cast<double>(h.w)));
+        }
+    } else {
+        for (int t = 0; t < k; ++t)
+            pred = __dadd_rn(pred, __dmul_rn(static_cast<double>(W.p[i * W.si + t * W.st]),
+                                             static_cast<double>(H.p[j * H.si + t * H.st])));
+    }
+    return pred;
+}
+
+template <bool IDX16, bool VEC>
 __global__ void unit_loss_kernel(const Unit* __restrict__ units, const int32_t* __restrict__ unit_panel,
                                  const int32_t* __restrict__ panel_base, const void* __restrict__ idx,
                                  const float* __restrict__ A, int32_t n_units, int32_t sentinel,
@@ -58,12 +81,7 @@ __global__ void unit_loss_kernel(const Unit* __restrict__ units, const int32_t* 
         for (int64_t e = U.e0 + lane; e < static_cast<int64_t>(U.e0) + U.len; e += 32) {
             const int g = IDX16 ? static_cast<const uint16_t*>(idx)[e] : static_cast<const int32_t*>(idx)[e];
             if (g == sentinel) continue;
-            const int64_t j = gb + g;
-            double pred = 0.0;
-            for (int t = 0; t < k; ++t)
-                pred = __dadd_rn(pred, __dmul_rn(static_cast<double>(W.p[i * W.si + t * W.st]),
-                                                 static_cast<double>(H.p[j * H.si + t * H.st])));
-            const double err = static_cast<double>(A[e]) - pred;
+            const double err = static_cast<double>(A[e]) - dot_double<VEC>(W, i, H, gb + g, k);
             acc += err * err;
         }
         acc = warp_sum(acc);
@@ -127,13 +145,21 @@ void launch_unit_loss(const DevSweep& L, const float* A, int32_t row_off, Factor
                       int k, double* unit_loss, cudaStream_t stream) {
     if (L.n_units == 0) return;
     const int threads = 256;
-    const int blocks = static_cast<int>(std::min<int64_t>((static_cast<int64_t>(L.n_units) * 32 + threads - 1) / threads, 8192));
-    if (L.idx16)
-        unit_loss_kernel<true><<<blocks, threads, 0, stream>>>(L.units, L.unit_panel, L.panel_base, L.idx, A,
-                                                                L.n_units, L.sentinel, row_off, W, H, k, unit_loss);
-    else
-        unit_loss_kernel<false><<<blocks, threads, 0, stream>>>(L.units, L.unit_panel, L.panel_base, L.idx, A,
-                                                                 L.n_units, L.sentinel, row_off, W, H, k, unit_loss);
+    const int blocks =
+        static_cast<int>(std::min<int64_t>((static_cast<int64_t>(L.n_units) * 32 + threads - 1) / threads, 8192));
+    const bool vec = W.st == 1 && H.st == 1 && k % 4 == 0 && W.si == k && H.si == k &&
+                     (reinterpret_cast<uintptr_t>(W.p) & 15) == 0 && (reinterpret_cast<uintptr_t>(H.p) & 15) == 0;
+#define PMF_LOSS(I16, V)                                                                                        \
+    unit_loss_kernel<I16, V><<<blocks, threads, 0, stream>>>(L.units, L.unit_panel, L.panel_base, L.idx, A, \
+                                                             L.n_units, L.sentinel, row_off, W, H, k, unit_loss)
+    if (L.idx16) {
+        if (vec) PMF_LOSS(true, true);
+        else PMF_LOSS(true, false);
+    } else {
+        if (vec) PMF_LOSS(false, true);
+        else PMF_LOSS(false, false);
+    }
+#undef PMF_LOSS
 }
 
 void launch_sum(const double* x, int64_t n, double* scratch, double* out, cudaStream_t stream) {

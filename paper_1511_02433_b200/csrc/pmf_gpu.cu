@@ -270,6 +270,10 @@ struct Ctx {
     double* unit_loss = nullptr;
     double* red_scratch = nullptr;
     double* red_out = nullptr;  // [0] loss, [1] reg W, [2] reg H, [3] probe sse
+    DevMem rm_mem;              // row-major copies of the CCD++ factors for the metric kernels
+    float* w_rm = nullptr;
+    float* h_rm = nullptr;
+    size_t rm_floats = 0;
     DevTriplet* probe = nullptr;
     int64_t n_probe = 0;
     DevMem probe_mem;
@@ -884,7 +888,22 @@ FactorView hview(const Ctx& c) {
 void metrics(Ctx& c, double* objective, double* rmse, double* train_rmse) {
     if (c.mode == 0) invalid("no model: call ccdpp_begin or als_begin first");
     CUDA_TRY(cudaSetDevice(c.device));
-    const FactorView W = wview(c), H = hview(c);
+    FactorView W = wview(c), H = hview(c);
+    if (c.mode == 1) {
+        // CCD++ keeps the factors column-major (k vectors); the per-entry dots read rows, so the
+        // metric kernels see row-major copies (same values, same t order, 4x fewer sector reads)
+        const size_t need = (static_cast<size_t>(c.ext_m) + c.ext_n) * c.k;
+        if (need != c.rm_floats) {
+            c.rm_mem.free_all();
+            c.w_rm = c.rm_mem.alloc<float>(static_cast<size_t>(c.ext_m) * c.k, false);
+            c.h_rm = c.rm_mem.alloc<float>(static_cast<size_t>(c.ext_n) * c.k, false);
+            c.rm_floats = need;
+        }
+        launch_transpose(c.W, c.ldm, c.k, c.ext_m, c.w_rm, c.stream);
+        launch_transpose(c.H, c.ldn, c.k, c.ext_n, c.h_rm, c.stream);
+        W = FactorView{c.w_rm, c.k, 1};
+        H = FactorView{c.h_rm, c.k, 1};
+    }
     launch_unit_loss(c.csr, c.A_csr, c.rank * c.Bm, W, H, c.k, c.unit_loss, c.stream);
     launch_sum(c.unit_loss, c.csr.n_units, c.red_scratch, c.red_out + 0, c.stream);
     const int64_t wn = c.mode == 1 ? static_cast<int64_t>(c.k) * c.ldm : static_cast<int64_t>(c.ext_m + 1) * c.k;
