@@ -138,8 +138,15 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
     for (auto& t : ts) t.join();
 }
 
+double now_s();
+double g_alloc_s = 0, g_h2d_s = 0;  // PMF_VERBOSE setup breakdown (host seconds in cudaMalloc / staged_h2d)
+
 // Host -> device on stream s (returns once the host data has been consumed).
 void staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    struct Clock {
+        double t0 = now_s();
+        ~Clock() { g_h2d_s += now_s() - t0; }
+    } clk;
     if (bytes < kStageMin) {
         CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
         return;
@@ -193,7 +200,9 @@ struct DevMem {
     T* alloc(size_t count, bool zero = true) {
         void* p = nullptr;
         if (count == 0) count = 1;
+        const double t0 = now_s();
         CUDA_TRY(cudaMalloc(&p, count * sizeof(T)));
+        g_alloc_s += now_s() - t0;
         blocks.push_back(p);
         if (zero) CUDA_TRY(cudaMemset(p, 0, count * sizeof(T)));
         return static_cast<T*>(p);
@@ -469,9 +478,10 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     if (std::getenv("PMF_VERBOSE"))
         std::fprintf(stderr,
                      "[pmf] ctx setup %.3f s: device init %.3f, csr layout %.3f, csr upload %.3f (csc layout "
-                     "in parallel), csc wait %.3f, csc upload %.3f, rest %.3f\n",
+                     "in parallel), csc wait %.3f, csc upload %.3f, rest %.3f; process totals: cudaMalloc %.3f, "
+                     "staged h2d %.3f\n",
                      c->setup_seconds, t_layout - t0, t_upload - t_layout, t_csr - t_upload, t_csc - t_csr,
-                     t_done - t_csc, now_s() - t_done);
+                     t_done - t_csc, now_s() - t_done, g_alloc_s, g_h2d_s);
     return c;
 }
 
