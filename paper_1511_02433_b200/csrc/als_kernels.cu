@@ -23,6 +23,16 @@ namespace {
 
 constexpr int kAlsThreads = 256;
 constexpr int kAlsWarps = kAlsThreads / 32;
+// tensor-core gram kernel: 4-warp CTAs, 5 per SM (20 warps, <= 96 registers; the gram aliases the
+// stage so the shared-memory footprint allows it)
+#ifndef PMF_TC_THREADS
+#define PMF_TC_THREADS 128
+#endif
+#ifndef PMF_TC_MINB
+#define PMF_TC_MINB 5
+#endif
+constexpr int kTcThreads = PMF_TC_THREADS;
+constexpr int kTcWarps = kTcThreads / 32;
 
 template <int KMAX>
 struct Tile {
@@ -458,9 +468,9 @@ struct TcGeo {
     static constexpr int GS0 = (KMAX + 1 + 3) & ~3;
     static constexpr int GS = (GS0 % 8 == 0) ? GS0 + 4 : GS0;
     static constexpr int GRAM = KMAX * GS + 2 * KMAX;
-    // staged rows and the gram are separate regions: the rows arrive by TMA bulk copies (async
-    // proxy) and the padding columns of X stay zero for the kernel's lifetime
-    static constexpr int WARP_FLOATS = (STAGE + GRAM + 64 + 31) & ~31;  // 128-byte aligned stages (TMA)
+    // the gram aliases the stage (it is formed after the unit's last chunk is consumed): a warp's
+    // footprint is max(stage, gram) + 64 floats, 128-byte aligned for the TMA destinations
+    static constexpr int WARP_FLOATS = ((STAGE > GRAM ? STAGE : GRAM) + 64 + 31) & ~31;
     static constexpr int count_tiles() {
         int c = 0;
         for (int mi = 0; mi < MT; ++mi)
@@ -490,7 +500,7 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
 }
 
 template <int NT, int MT>
-__global__ void __launch_bounds__(kAlsThreads)
+__global__ void __launch_bounds__(kTcThreads, PMF_TC_MINB)
 als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_t* __restrict__ idx,
                    const float* __restrict__ val, const float* __restrict__ opp, float* __restrict__ out,
                    int32_t out_off, int k, float lambda, int weighted, float* __restrict__ partial,
@@ -500,18 +510,19 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
     constexpr int KS = T::KS, JN = T::JN, NTILES = T::NTILES, KMAX = T::KMAX;
     constexpr int GS = T::GS;
     extern __shared__ __align__(128) float smem[];
-    __shared__ __align__(8) uint64_t s_bar[kAlsWarps];
+    __shared__ __align__(8) uint64_t s_bar[kTcWarps];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
     const int g = lane >> 2, tig = lane & 3;
     float* X = smem + warp * T::WARP_FLOATS;
-    float* G = X + T::STAGE;
+    float* G = X;  // aliases the stage
     int* sidx = reinterpret_cast<int*>(X + T::WARP_FLOATS - 64);
     float* sval = X + T::WARP_FLOATS - 32;
     uint64_t* bar = &s_bar[warp];
     uint32_t phase = 0;
     if (tma) {
-        // TMA rows (4k bytes each) leave columns [k, KS) untouched: zero them once
+        // TMA rows (4k bytes each) leave columns [k, KS) untouched: zero them here (and per unit after
+        // the aliased gram has overwritten them)
         for (int e = lane; e < T::STAGE; e += 32) X[e] = 0.f;
         if (lane == 0) {
             asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
@@ -534,6 +545,12 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
 #pragma unroll
         for (int t = 0; t < MT; ++t) accr[t][0] = accr[t][1] = accr[t][2] = accr[t][3] = 0.f;
         float rhs0 = 0.f, rhs1 = 0.f;
+        if (tma == 1 && KS != k) {
+            // per-row bulk copies write k columns: re-zero the padding columns the previous unit's
+            // gram (aliasing the stage) overwrote
+            __syncwarp();
+            for (int e = lane; e < 32 * (KS - k); e += 32) X[(e / (KS - k)) * KS + k + e % (KS - k)] = 0.f;
+        }
         for (int base = 0; base < U.len; base += 32) {
             const int cnt = min(32, U.len - base);
             const int cnt8 = (cnt + 7) & ~7;
@@ -806,7 +823,7 @@ size_t smem_for() {
 
 template <int NT, int MT>
 size_t smem_for_tc() {
-    return static_cast<size_t>(kAlsWarps) * TcGeo<NT, MT>::WARP_FLOATS * sizeof(float);
+    return static_cast<size_t>(kTcWarps) * TcGeo<NT, MT>::WARP_FLOATS * sizeof(float);
 }
 
 bool use_tensor_cores() {
@@ -861,14 +878,14 @@ void launch_tc(const DevAls& L, const float* opp, int64_t n_opp, float* out, int
                bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t s) {
     const size_t sm = smem_for_tc<NT, MT>();
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_gram_tc_kernel<NT, MT>, kAlsThreads, sm);
-    const int blocks = std::max(1, std::min<int>(per_sm * sm_count, (L.n_units + kAlsWarps - 1) / kAlsWarps));
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_gram_tc_kernel<NT, MT>, kTcThreads, sm);
+    const int blocks = std::max(1, std::min<int>(per_sm * sm_count, (L.n_units + kTcWarps - 1) / kTcWarps));
     // TMA row staging needs 16-byte rows (k % 4 == 0; the factor base is cudaMalloc-aligned)
     const int mode = als_tma_mode();
     int tma = mode != 0 && k % 4 == 0 && (reinterpret_cast<uintptr_t>(opp) & 15) == 0 ? 1 : 0;
     alignas(64) CUtensorMap map{};
     if (tma && mode == 2 && k == TcGeo<NT, MT>::KS && make_rows_map(&map, opp, n_opp, k)) tma = 2;
-    als_gram_tc_kernel<NT, MT><<<blocks, kAlsThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off,
+    als_gram_tc_kernel<NT, MT><<<blocks, kTcThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off,
                                                                 k, lambda, weighted ? 1 : 0, L.partial, d_counter,
                                                                 d_status, tma, als_exact_chol(), map);
 }
