@@ -329,6 +329,28 @@ __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
     return true;
 }
 
+// One Gauss-Seidel sweep over t = 0..k-1 on (G + lambda I) x = b from the current x: the item/user-wise
+// CCD coordinate update (ccd.hpp:56-80).  With R_ij = a_ij - sum_t' x_t' h_jt', the reference's
+// z* = sum_j (R_ij + x_t h_jt) h_jt / (lambda + sum_j h_jt^2) equals (b_t - sum_{t' != t} G_tt' x_t') /
+// (lambda + G_tt), so the epoch needs the per-row gram (the ALS gram, on the tensor cores) and no
+// residual.  G rows are read along the lanes (conflict-free); den == 0 -> 0 as in the reference.
+template <int KMAX, int GS>
+__device__ __forceinline__ void warp_gauss_seidel(const float* G, int k, float b0, float b1, float& x0, float& x1) {
+    const int lane = threadIdx.x & 31;
+    for (int t = 0; t < k; ++t) {
+        const float* Gt = G + t * GS;
+        float p = (lane < k && lane != t) ? Gt[lane] * x0 : 0.f;
+        if (KMAX > 32 && lane + 32 < k && lane + 32 != t) p = fmaf(Gt[lane + 32], x1, p);
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) p += __shfl_xor_sync(0xffffffffu, p, off);
+        const float bt = __shfl_sync(0xffffffffu, t < 32 ? b0 : b1, t & 31);
+        const float den = Gt[t];
+        const float z = den == 0.f ? 0.f : __fdiv_rn(bt - p, den);
+        if (t < 32) x0 = lane == t ? z : x0;
+        else x1 = lane + 32 == t ? z : x1;
+    }
+}
+
 // Stages the gathered opposing rows of one 32-entry chunk into X[s][0..KS): lanes own features
 // (coalesced 4k-byte row reads), 8 rows' loads are issued before they are stored (bank-conflict
 // free stores); columns [k, KS) and rows [cnt, rows_pad) are zero.
@@ -504,7 +526,7 @@ __global__ void __launch_bounds__(kTcThreads, PMF_TC_MINB)
 als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_t* __restrict__ idx,
                    const float* __restrict__ val, const float* __restrict__ opp, float* __restrict__ out,
                    int32_t out_off, int k, float lambda, int weighted, float* __restrict__ partial,
-                   int* __restrict__ counter, int* __restrict__ status, int tma, int exact,
+                   int* __restrict__ counter, int* __restrict__ status, int tma, int exact, int gs,
                    const __grid_constant__ CUtensorMap rows_map) {
     using T = TcGeo<NT, MT>;
     constexpr int KS = T::KS, JN = T::JN, NTILES = T::NTILES, KMAX = T::KMAX;
@@ -716,6 +738,15 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
             continue;
         }
         __syncwarp();
+        float* dst = out + static_cast<int64_t>(out_off + U.o) * k;
+        if (gs) {  // item/user-wise CCD: one coordinate sweep from the current row
+            float x0 = lane < k ? dst[lane] : 0.f, x1 = lane + 32 < k ? dst[lane + 32] : 0.f;
+            warp_gauss_seidel<KMAX, GS>(G, k, rhs0, rhs1, x0, x1);
+            if (lane < k) dst[lane] = x0;
+            if (lane + 32 < k) dst[lane + 32] = x1;
+            __syncwarp();
+            continue;
+        }
         const bool ok = exact == 2 ? true  // timing experiment only (PMF_ALS_EXACT=2): no factorisation
                         : (exact && k == KMAX) ? warp_cholesky_solve_exact<KMAX, GS>(G, rhs0, rhs1)
                                                : warp_cholesky_solve_v4<KMAX, GS>(G, k, rhs0, rhs1);
@@ -723,7 +754,6 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
             if (lane == 0) atomicExch(status, 4);
             rhs0 = rhs1 = 0.f;
         }
-        float* dst = out + static_cast<int64_t>(out_off + U.o) * k;
         if (lane < k) dst[lane] = rhs0;
         if (lane + 32 < k) dst[lane + 32] = rhs1;
         __syncwarp();
@@ -734,7 +764,7 @@ template <int KMAX>
 __global__ void __launch_bounds__(kAlsThreads)
 als_reduce_solve_kernel(const int32_t* __restrict__ mo_out, const int32_t* __restrict__ mo_start,
                         int32_t n_mo, const float* __restrict__ partial, float* __restrict__ out,
-                        int32_t out_off, int k, float lambda, int weighted, int* __restrict__ status) {
+                        int32_t out_off, int k, float lambda, int weighted, int* __restrict__ status, int gs) {
     using T = Tile<KMAX>;
     constexpr int GS = T::GS;
     extern __shared__ float smem[];
@@ -764,12 +794,16 @@ als_reduce_solve_kernel(const int32_t* __restrict__ mo_out, const int32_t* __res
         const float ridge = weighted ? lambda * cntf : lambda;
         for (int d = lane; d < k; d += 32) G[d * GS + d] += ridge;
         __syncwarp();
-        const bool ok = warp_cholesky_solve<KMAX>(G, k, b0, b1);
-        if (!ok) {
+        float* dst = out + static_cast<int64_t>(out_off + mo_out[q]) * k;
+        if (gs) {
+            float x0 = lane < k ? dst[lane] : 0.f, x1 = lane + 32 < k ? dst[lane + 32] : 0.f;
+            warp_gauss_seidel<KMAX, GS>(G, k, b0, b1, x0, x1);
+            b0 = x0;
+            b1 = x1;
+        } else if (!warp_cholesky_solve<KMAX>(G, k, b0, b1)) {
             if (lane == 0) atomicExch(status, 4);
             b0 = b1 = 0.f;
         }
-        float* dst = out + static_cast<int64_t>(out_off + mo_out[q]) * k;
         if (lane < k) dst[lane] = b0;
         if (lane + 32 < k) dst[lane + 32] = b1;
         __syncwarp();
@@ -875,7 +909,7 @@ int als_tma_mode() {
 
 template <int NT, int MT>
 void launch_tc(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k, float lambda,
-               bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t s) {
+               bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t s, bool gs) {
     const size_t sm = smem_for_tc<NT, MT>();
     int per_sm = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_gram_tc_kernel<NT, MT>, kTcThreads, sm);
@@ -887,12 +921,12 @@ void launch_tc(const DevAls& L, const float* opp, int64_t n_opp, float* out, int
     if (tma && mode == 2 && k == TcGeo<NT, MT>::KS && make_rows_map(&map, opp, n_opp, k)) tma = 2;
     als_gram_tc_kernel<NT, MT><<<blocks, kTcThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off,
                                                                 k, lambda, weighted ? 1 : 0, L.partial, d_counter,
-                                                                d_status, tma, als_exact_chol(), map);
+                                                                d_status, tma, als_exact_chol(), gs ? 1 : 0, map);
 }
 
 template <int KMAX>
 int launch_k(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k, float lambda, bool weighted,
-             int* d_counter, int* d_status, int sm_count, cudaStream_t s) {
+             int* d_counter, int* d_status, int sm_count, cudaStream_t s, bool gs) {
     int launched = 0;
     const size_t sm = smem_for<KMAX>();
     if (L.n_units > 0) {
@@ -901,7 +935,7 @@ int launch_k(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32
             // N tiles (8 features) and M tiles (16 features) covering the k features
             const int nt = (k + 7) / 8, mt = (k + 15) / 16;
 #define PMF_TC(NT_, MT_) \
-    if (nt == NT_ && mt == MT_) launch_tc<NT_, MT_>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, s)
+    if (nt == NT_ && mt == MT_) launch_tc<NT_, MT_>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, s, gs)
             PMF_TC(1, 1); else PMF_TC(2, 1); else PMF_TC(3, 1); else PMF_TC(3, 2); else PMF_TC(4, 2);
             else PMF_TC(5, 2); else PMF_TC(5, 3); else PMF_TC(6, 3);
 #undef PMF_TC
@@ -918,7 +952,8 @@ int launch_k(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32
     if (L.n_mo > 0) {
         const int blocks = std::max(1, std::min(4 * sm_count, (L.n_mo + kAlsWarps - 1) / kAlsWarps));
         als_reduce_solve_kernel<KMAX><<<blocks, kAlsThreads, sm, s>>>(L.mo_out, L.mo_start, L.n_mo, L.partial, out,
-                                                                       out_off, k, lambda, weighted ? 1 : 0, d_status);
+                                                                       out_off, k, lambda, weighted ? 1 : 0, d_status,
+                                                                       gs ? 1 : 0);
         ++launched;
     }
     if (L.n_empty > 0) {
@@ -963,13 +998,20 @@ void als_set_attributes() {
     set_attr_k<64>();
 }
 
+bool als_gram_gs_supported(int k) { return use_tensor_cores() && k >= 1 && k <= 40; }
+
 int launch_als_half(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k,
-                    float lambda, bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t stream) {
-    if (k <= 8) return launch_k<8>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
-    if (k <= 16) return launch_k<16>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
-    if (k <= 32) return launch_k<32>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
-    if (k <= 40) return launch_k<40>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
-    return launch_k<64>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream);
+                    float lambda, bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t stream,
+                    bool gs) {
+    if (gs && !als_gram_gs_supported(k)) return -1;  // the Gauss-Seidel solve lives in the tensor-core path
+#define PMF_HALF(K) \
+    return launch_k<K>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream, gs)
+    if (k <= 8) PMF_HALF(8);
+    if (k <= 16) PMF_HALF(16);
+    if (k <= 32) PMF_HALF(32);
+    if (k <= 40) PMF_HALF(40);
+    PMF_HALF(64);
+#undef PMF_HALF
 }
 
 void launch_cholesky_batched(float* a, float* x, int batch, int k, int* d_status, cudaStream_t s) {

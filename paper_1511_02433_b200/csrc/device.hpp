@@ -146,9 +146,12 @@ struct DevAls {
 // Solves every output row of one side: out row (out_off + o) of the row-major factor `out`
 // (stride k) from the row-major opposing factor `opp` (n_opp addressable rows).  status: device int
 // set to 4 on a non-positive pivot.  Returns kernels launched.
+// gs: item/user-wise CCD instead of ALS -- one Gauss-Seidel sweep on (G + lambda I) x = b starting
+// from the current rows of `out` (needs als_gram_gs_supported(k); returns -1 otherwise).
 int launch_als_half(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k,
                     float lambda, bool weighted, int* d_counter, int* d_status, int sm_count,
-                    cudaStream_t stream);
+                    cudaStream_t stream, bool gs = false);
+bool als_gram_gs_supported(int k);
 void als_set_attributes();
 // Batched Cholesky factor + solve of `batch` k*k row-major systems in place.
 void launch_cholesky_batched(float* a, float* x, int batch, int k, int* d_status,

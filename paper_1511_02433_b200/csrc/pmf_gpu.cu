@@ -270,6 +270,7 @@ struct Ctx {
     DevMem ccdw_mem;   // item/user-wise CCD workspace
     CcdWs ccdw;
     bool ccdw_on = false;
+    bool ccdw_gram = false;  // item/user-wise CCD as gram + Gauss-Seidel sweeps (no residual)
     DevAls als_csr, als_csc;
     int* d_counter = nullptr;
     int* d_status = nullptr;
@@ -837,6 +838,21 @@ void ccdw_begin(Ctx& c, const pmf_ccd_config* cfg) {
     c.ccdw_mem.free_all();
     c.k = cfg->k;
     c.lambda = cfg->lambda;
+    // k <= 40: each row's (column's) coordinate sweep is one Gauss-Seidel sweep on its normal
+    // equations, whose gram and right-hand side come off the ALS tensor-core gram kernel; otherwise
+    // (or PMF_CCD_RESIDUAL) the residual-based warp-per-row / CTA-per-column kernels
+    c.ccdw_gram = als_gram_gs_supported(c.k) && std::getenv("PMF_CCD_RESIDUAL") == nullptr;
+    if (c.ccdw_gram) {
+        c.W = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_m + 1) * c.k);  // W = 0 (ccd.hpp:323)
+        c.H = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_n + 1) * c.k);
+        als_alloc_partials(c, c.k);
+        const auto H = init_items_host(c.n, cfg->k, cfg->seed);  // model.hpp:86-93
+        upload_rowmajor(c, c.H, c.ext_n, H.data(), c.n, cfg->k, false);
+        CUDA_TRY(cudaGetLastError());
+        c.mode = 2;
+        c.ccdw_on = true;
+        return;
+    }
     CcdWs& w = c.ccdw;
     w.m = c.m;
     w.n = c.n;
@@ -872,7 +888,16 @@ void ccdw_iterate(Ctx& c, int n_outer, double* secs) {
     CUDA_TRY(cudaEventCreate(&e1));
     for (int it = 0; it < n_outer; ++it) {
         CUDA_TRY(cudaEventRecord(e0, c.stream));
-        c.launches_per_iter = launch_ccd_epoch(c.ccdw, c.W, c.H, c.k, c.lambda, c.stream);
+        if (c.ccdw_gram) {  // W sweep with H fixed, then H sweep with the new W (ccd.hpp:113-119)
+            const int a = launch_als_half(c.als_csr, c.H, c.ext_n, c.W, 0, c.k, c.lambda, false, c.d_counter,
+                                          c.d_status, c.sm_count, c.stream, true);
+            const int b = launch_als_half(c.als_csc, c.W, c.ext_m, c.H, 0, c.k, c.lambda, false, c.d_counter + 1,
+                                          c.d_status, c.sm_count, c.stream, true);
+            if (a < 0 || b < 0) throw PmfError(PMF_RUNTIME_ERROR, "item/user-wise CCD: gram path unavailable");
+            c.launches_per_iter = a + b;
+        } else {
+            c.launches_per_iter = launch_ccd_epoch(c.ccdw, c.W, c.H, c.k, c.lambda, c.stream);
+        }
         CUDA_TRY(cudaEventRecord(e1, c.stream));
         CUDA_TRY(cudaEventSynchronize(e1));
         float ms = 0;

@@ -1,7 +1,8 @@
 """GPU item/user-wise CCD (ccd.hpp:52-125, ccd_train :310-344) against the oracle
 (pinned to the reference in test_ccd_oracle.py): per-iteration objective, train and probe RMSE within
-1e-4 relative, factors within 1e-3 relative Frobenius (sums over a row / column are warp / CTA trees,
-the reference's are sequential), objective non-increasing, edge cases."""
+1e-4 relative, factors within 1e-3 relative Frobenius (k <= 40: each coordinate sweep is a Gauss-Seidel
+sweep on the row's normal equations with a tensor-core gram; k > 40: warp / CTA residual sweeps; the
+reference's sums are sequential), objective non-increasing, edge cases, both paths."""
 import numpy as np
 import pytest
 
@@ -56,3 +57,21 @@ def test_ccd_long_rows_vs_oracle(pmf, oracle):
     for r, g in zip(rep.rows, rows):
         assert rel(r.objective, g["objective"]) < 1e-4
     assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+
+
+def test_ccd_paths_vs_oracle(pmf, oracle, ml100k, monkeypatch):
+    # k <= 40 runs the gram + Gauss-Seidel path; k > 40 (or PMF_CCD_RESIDUAL) the residual kernels
+    train, probe = ml100k
+    A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
+    O = oracle.from_triplets(train, 943, 1682)
+    for k, residual in ((12, True), (44, False)):
+        if residual:
+            monkeypatch.setenv("PMF_CCD_RESIDUAL", "1")
+        else:
+            monkeypatch.delenv("PMF_CCD_RESIDUAL", raising=False)
+        model, rep = pmf.ccd_train(pmf.CcdConfig(k=k, lam=0.1, outer_iters=2, inner_iters=1, seed=3), A, probe)
+        W, H, rows = oracle.ccd_train(O, k, 0.1, 2, 3, probe)
+        for r, g in zip(rep.rows, rows):
+            assert rel(r.objective, g["objective"]) < 1e-4
+            assert rel(r.rmse, g["rmse"]) < 1e-4
+        assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
