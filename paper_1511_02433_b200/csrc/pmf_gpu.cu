@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <future>
+#include <map>
 #include <mutex>
 #include <thread>
 #include <memory>
@@ -194,16 +195,81 @@ void staged_d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
 }
 
 // ---- device memory -----------------------------------------------------------------------------
+// Process-wide cache of device blocks (a caching allocator, as deep-learning runtimes keep): a
+// context's blocks come back here when it is destroyed and serve the next context's allocations of
+// the same size class, so creating and destroying contexts does not pay cudaFree -- which
+// synchronises the device and was measured at up to 0.7 s for 411 MB blocks when the driver releases
+// the memory (scripts/micro/malloc_cost.cu) -- inside a caller's timed region.  PMF_NO_ALLOC_CACHE=1
+// turns it off; a failing cudaMalloc flushes the cache and retries.
+struct BlockCache {
+    std::mutex mu;
+    std::multimap<std::pair<int, size_t>, void*> blocks;  // (device, bytes) -> block
+    static bool enabled() {
+        static const bool on = std::getenv("PMF_NO_ALLOC_CACHE") == nullptr;
+        return on;
+    }
+    static size_t size_class(size_t b) {
+        const size_t g = b < (size_t(1) << 20) ? 512 : (size_t(2) << 20);
+        return (b + g - 1) / g * g;
+    }
+    // a cached block of the class or up to 1/4 larger; returns its size in *got
+    void* take(int dev, size_t bytes, size_t* got) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = blocks.lower_bound({dev, bytes});
+        if (it == blocks.end() || it->first.first != dev || it->first.second > bytes + bytes / 4) return nullptr;
+        void* p = it->second;
+        *got = it->first.second;
+        blocks.erase(it);
+        return p;
+    }
+    void give(int dev, size_t bytes, void* p) {
+        std::lock_guard<std::mutex> lk(mu);
+        blocks.emplace(std::make_pair(dev, bytes), p);
+    }
+    void flush() {
+        std::lock_guard<std::mutex> lk(mu);
+        int cur = 0;
+        cudaGetDevice(&cur);
+        for (auto& kv : blocks) {
+            cudaSetDevice(kv.first.first);
+            cudaFree(kv.second);
+        }
+        blocks.clear();
+        cudaSetDevice(cur);
+    }
+};
+BlockCache& block_cache() {
+    static BlockCache* c = new BlockCache();  // never destroyed: blocks live until process exit
+    return *c;
+}
+
 struct DevMem {
-    std::vector<void*> blocks;
+    struct Block {
+        void* p;
+        size_t bytes;
+        int dev;
+    };
+    std::vector<Block> blocks;
     template <class T>
     T* alloc(size_t count, bool zero = true) {
-        void* p = nullptr;
         if (count == 0) count = 1;
         const double t0 = now_s();
-        CUDA_TRY(cudaMalloc(&p, count * sizeof(T)));
+        int dev = 0;
+        CUDA_TRY(cudaGetDevice(&dev));
+        const bool cache = BlockCache::enabled();
+        size_t bytes = cache ? BlockCache::size_class(count * sizeof(T)) : count * sizeof(T);
+        void* p = cache ? block_cache().take(dev, bytes, &bytes) : nullptr;
+        if (!p) {
+            cudaError_t e = cudaMalloc(&p, bytes);
+            if (e == cudaErrorMemoryAllocation && cache) {
+                cudaGetLastError();
+                block_cache().flush();
+                e = cudaMalloc(&p, bytes);
+            }
+            CUDA_TRY(e);
+        }
         g_alloc_s += now_s() - t0;
-        blocks.push_back(p);
+        blocks.push_back(Block{p, bytes, dev});
         if (zero) CUDA_TRY(cudaMemset(p, 0, count * sizeof(T)));
         return static_cast<T*>(p);
     }
@@ -222,7 +288,24 @@ struct DevMem {
         return p;
     }
     void free_all() {
-        for (void* p : blocks) cudaFree(p);
+        if (blocks.empty()) return;
+        if (!BlockCache::enabled()) {
+            for (const Block& b : blocks) cudaFree(b.p);
+            blocks.clear();
+            return;
+        }
+        // kernels still in flight may use the blocks: the devices go idle before the blocks are reused
+        int cur = 0;
+        cudaGetDevice(&cur);
+        int synced = -1;
+        for (const Block& b : blocks)
+            if (b.dev != synced) {
+                cudaSetDevice(b.dev);
+                cudaDeviceSynchronize();
+                synced = b.dev;
+            }
+        cudaSetDevice(cur);
+        for (const Block& b : blocks) block_cache().give(b.dev, b.bytes, b.p);
         blocks.clear();
     }
     ~DevMem() { free_all(); }
