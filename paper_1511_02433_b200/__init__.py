@@ -101,6 +101,7 @@ _SIGS = {
     "pmf_last_error": ([], C.c_char_p),
     "pmf_abi_version": ([], C.c_int32),
     "pmf_device_count": ([], C.c_int32),
+    "pmf_release_cached_memory": ([C.c_void_p], C.c_int),
     "pmf_ccdpp_train": ([_P, _P, _P, C.c_int64, _P, _P, _P, _P], C.c_int),
     "pmf_als_train": ([_P, _P, _P, C.c_int64, _P, _P, _P, _P], C.c_int),
     "pmf_ccd_train": ([_P, _P, _P, C.c_int64, _P, _P, _P, _P], C.c_int),
@@ -185,6 +186,13 @@ def _check(status: int):
 
 def device_count() -> int:
     return int(lib.pmf_device_count())
+
+
+def release_cached_memory() -> int:
+    """Returns the device blocks cached from destroyed contexts to the driver; bytes released."""
+    n = C.c_int64(0)
+    _check(lib.pmf_release_cached_memory(C.byref(n)))
+    return int(n.value)
 
 
 def _as_triplets(t) -> np.ndarray:

@@ -226,16 +226,19 @@ struct BlockCache {
         std::lock_guard<std::mutex> lk(mu);
         blocks.emplace(std::make_pair(dev, bytes), p);
     }
-    void flush() {
+    int64_t flush() {
         std::lock_guard<std::mutex> lk(mu);
         int cur = 0;
         cudaGetDevice(&cur);
+        int64_t bytes = 0;
         for (auto& kv : blocks) {
             cudaSetDevice(kv.first.first);
             cudaFree(kv.second);
+            bytes += static_cast<int64_t>(kv.first.second);
         }
         blocks.clear();
         cudaSetDevice(cur);
+        return bytes;
     }
 };
 BlockCache& block_cache() {
@@ -1166,6 +1169,13 @@ extern "C" {
 
 const char* pmf_last_error(void) { return g_err.c_str(); }
 int32_t pmf_abi_version(void) { return PMF_ABI_VERSION; }
+pmf_status pmf_release_cached_memory(int64_t* released) {
+    return guard([&] {
+        const int64_t b = block_cache().flush();
+        if (released) *released = b;
+    });
+}
+
 int32_t pmf_device_count(void) {
     int c = 0;
     if (cudaGetDeviceCount(&c) != cudaSuccess) {

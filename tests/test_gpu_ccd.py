@@ -261,3 +261,16 @@ def test_split_promote_wide_panels_residual(pmf, oracle):
     pred = np.einsum("ik,ik->i", model.w[ri].astype(np.float64), model.h[O.col_of].astype(np.float64))
     assert np.max(np.abs(rr - (O.val_row - pred))) < 1e-4
     ctx.close()
+
+
+def test_release_cached_memory(pmf, ml100k):
+    """Destroyed contexts' device blocks are cached (no cudaFree in the next call) and returned to the
+    driver on request; training after the release allocates afresh and gives the same model."""
+    train, probe = ml100k
+    A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
+    cfg = pmf.CcdConfig(k=5, lam=0.05, outer_iters=2, inner_iters=3, seed=2)
+    m1, _ = pmf.ccdpp_train(cfg, A, probe)
+    assert pmf.release_cached_memory() > 0
+    assert pmf.release_cached_memory() == 0
+    m2, _ = pmf.ccdpp_train(cfg, A, probe)
+    assert m1 == m2
