@@ -210,21 +210,33 @@ __device__ __forceinline__ bool warp_cholesky_solve_exact(float* G, float& b0, f
 
 // warp_cholesky_solve for the tensor-core kernels' gram (row stride GS: 16-byte rows, GS / 4 odd):
 // the lane's row and the pivot row are read 4 columns at a time with 128-bit loads (the pivot row is a
-// broadcast, the lanes' rows are conflict-free), and the second row set of a lane (i0 + 32) is only
-// visited while it exists (j < k - 33, warp-uniform).  Sums are formed in the same order as
-// warp_cholesky_solve, so the factor is bitwise the same.
+// broadcast, the lanes' rows are conflict-free), the second row set of a lane (i0 + 32) is only
+// visited while it exists (j < k - 33, warp-uniform), and each pivot comes from a running sum of its
+// row's squared L entries carried down the lanes instead of a dot product every lane repeats.
 template <int KMAX, int GS>
 __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
     static_assert(GS % 4 == 0 && (GS / 4) % 2 == 1, "row stride must be an odd multiple of 4 floats");
     const int lane = threadIdx.x & 31;
     float* Rinv = G + KMAX * GS;  // 1 / L_jj (the solves multiply instead of dividing)
     bool ok = true;
+    // running sum of squares of each row's finished L entries, carried by the lane that owns the
+    // row: the pivot is G_jj minus that sum (no per-lane recomputation of row j's squared norm);
+    // rows move down one lane per step, so the sums shift with them
+    float n0 = 0.f, n1 = 0.f;
     for (int j = 0; j < k; ++j) {
         const int i0 = j + 1 + lane, i1 = i0 + 32;
         const bool h0 = i0 < k;
         const float* Gj = G + j * GS;
         const float* G0 = G + (h0 ? i0 : j) * GS;
-        float d0 = Gj[j], d1 = 0.f, d2 = 0.f, d3 = 0.f;
+        const float nj = __shfl_sync(0xffffffffu, n0, 0);  // row j was lane 0's row at step j - 1
+        {
+            const float up0 = __shfl_down_sync(0xffffffffu, n0, 1);
+            const float wrap = __shfl_sync(0xffffffffu, n1, 0);
+            const float up1 = __shfl_down_sync(0xffffffffu, n1, 1);
+            n0 = j == 0 ? 0.f : (lane == 31 ? wrap : up0);
+            n1 = j == 0 ? 0.f : (lane == 31 ? 0.f : up1);
+        }
+        const float d = Gj[j] - nj;
         float s0 = h0 ? G0[j] : 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
         int t = 0;
         if (KMAX > 32 && j < k - 33) {  // some lanes own a second row i1
@@ -235,10 +247,6 @@ __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
                 const float4 g = *reinterpret_cast<const float4*>(Gj + t);
                 const float4 a = *reinterpret_cast<const float4*>(G0 + t);
                 const float4 c = *reinterpret_cast<const float4*>(G1 + t);
-                d0 = fmaf(-g.x, g.x, d0);
-                d1 = fmaf(-g.y, g.y, d1);
-                d2 = fmaf(-g.z, g.z, d2);
-                d3 = fmaf(-g.w, g.w, d3);
                 s0 = fmaf(-a.x, g.x, s0);
                 s1 = fmaf(-a.y, g.y, s1);
                 s2 = fmaf(-a.z, g.z, s2);
@@ -250,20 +258,21 @@ __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
             }
             for (; t < j; ++t) {
                 const float g0 = Gj[t];
-                d0 = fmaf(-g0, g0, d0);
                 s0 = fmaf(-G0[t], g0, s0);
                 r0 = fmaf(-G1[t], g0, r0);
             }
-            const float d = (d0 + d1) + (d2 + d3);
             if (!(d > 0.f)) {
                 ok = false;
                 break;
             }
             const float ljj = sqrtf(d);
             const float rl = 1.0f / ljj;
+            const float l0 = ((s0 + s1) + (s2 + s3)) * rl, l1 = (r0 + r1) * rl;
+            n0 = fmaf(l0, l0, n0);
+            n1 = fmaf(l1, l1, n1);
             __syncwarp();
-            if (h0) G[i0 * GS + j] = G[j * GS + i0] = ((s0 + s1) + (s2 + s3)) * rl;
-            if (h1) G[i1 * GS + j] = G[j * GS + i1] = (r0 + r1) * rl;
+            if (h0) G[i0 * GS + j] = G[j * GS + i0] = l0;
+            if (h1) G[i1 * GS + j] = G[j * GS + i1] = l1;
             if (lane == 0) {
                 G[j * GS + j] = ljj;
                 Rinv[j] = rl;
@@ -274,29 +283,22 @@ __device__ bool warp_cholesky_solve_v4(float* G, int k, float& b0, float& b1) {
         for (; t + 4 <= j; t += 4) {
             const float4 g = *reinterpret_cast<const float4*>(Gj + t);
             const float4 a = *reinterpret_cast<const float4*>(G0 + t);
-            d0 = fmaf(-g.x, g.x, d0);
-            d1 = fmaf(-g.y, g.y, d1);
-            d2 = fmaf(-g.z, g.z, d2);
-            d3 = fmaf(-g.w, g.w, d3);
             s0 = fmaf(-a.x, g.x, s0);
             s1 = fmaf(-a.y, g.y, s1);
             s2 = fmaf(-a.z, g.z, s2);
             s3 = fmaf(-a.w, g.w, s3);
         }
-        for (; t < j; ++t) {
-            const float g0 = Gj[t];
-            d0 = fmaf(-g0, g0, d0);
-            s0 = fmaf(-G0[t], g0, s0);
-        }
-        const float d = (d0 + d1) + (d2 + d3);
+        for (; t < j; ++t) s0 = fmaf(-G0[t], Gj[t], s0);
         if (!(d > 0.f)) {
             ok = false;
             break;
         }
         const float ljj = sqrtf(d);
         const float rl = 1.0f / ljj;
+        const float l0 = ((s0 + s1) + (s2 + s3)) * rl;
+        n0 = fmaf(l0, l0, n0);
         __syncwarp();
-        if (h0) G[i0 * GS + j] = G[j * GS + i0] = ((s0 + s1) + (s2 + s3)) * rl;
+        if (h0) G[i0 * GS + j] = G[j * GS + i0] = l0;
         if (lane == 0) {
             G[j * GS + j] = ljj;
             Rinv[j] = rl;
