@@ -256,9 +256,9 @@ pmf_status pmf_synth_ratings(int32_t m, int32_t n, int32_t true_rank, int64_t n_
 const char* pmf_last_error(void);
 int32_t pmf_abi_version(void);
 int32_t pmf_device_count(void);
-/* Device blocks of destroyed contexts stay cached for the next context (no cudaFree in a caller's
- * timed region); this returns them to the driver (no reference counterpart).  Bytes released in
- * *released (may be null). */
+/* Device blocks and page-locked host layout blocks of destroyed contexts stay cached for the next
+ * context (no cudaFree / re-pinning in a caller's timed region); this returns the idle ones to the
+ * driver (no reference counterpart).  Bytes released in *released (may be null). */
 pmf_status pmf_release_cached_memory(int64_t* released);
 
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink / NVSwitch) -------------------------- */

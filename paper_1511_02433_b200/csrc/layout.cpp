@@ -12,6 +12,12 @@
 
 namespace pmfgpu {
 
+HostAllocHooks& host_alloc_hooks() {
+    static HostAllocHooks h;
+    return h;
+}
+
+
 void parallel_for(int64_t n, const std::function<void(int64_t, int64_t)>& fn, int threads) {
     if (n <= 0) return;
     if (threads <= 0) threads = static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));

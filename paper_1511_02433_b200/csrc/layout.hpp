@@ -15,6 +15,7 @@
 #include <functional>
 #include <memory>
 #include <string>
+#include <utility>
 #include <vector>
 
 namespace pmfgpu {
@@ -38,22 +39,62 @@ struct UnitCost {
 };
 UnitCost unit_cost_model();
 
+// Optional allocator for large host buffers, installed by the device library: page-locked blocks
+// from a cache, so a layout is filled straight into DMA-able memory and uploaded without a staging
+// copy.  alloc returns nullptr to decline (the buffer then comes from operator new).
+struct HostAllocHooks {
+    void* (*alloc)(size_t bytes) = nullptr;
+    void (*free)(void* p, size_t bytes) = nullptr;
+    size_t min_bytes = size_t(16) << 20;
+};
+HostAllocHooks& host_alloc_hooks();
+
 // Uninitialised POD buffer (large layout arrays are filled in parallel; std::vector would first
 // value-initialise them serially).
 template <class T>
 struct PodBuf {
-    std::unique_ptr<T[]> p;
+    T* p = nullptr;
     size_t n = 0;
+    size_t bytes = 0;
+    bool hooked = false;
+    PodBuf() = default;
+    PodBuf(const PodBuf&) = delete;
+    PodBuf& operator=(const PodBuf&) = delete;
+    PodBuf(PodBuf&& o) noexcept { swap(o); }
+    PodBuf& operator=(PodBuf&& o) noexcept {
+        if (this != &o) {
+            reset();
+            swap(o);
+        }
+        return *this;
+    }
+    ~PodBuf() { reset(); }
+    void swap(PodBuf& o) noexcept {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+        std::swap(bytes, o.bytes);
+        std::swap(hooked, o.hooked);
+    }
     void alloc(size_t count) {
-        p.reset(new T[count ? count : 1]);
+        reset();
+        bytes = (count ? count : 1) * sizeof(T);
+        const HostAllocHooks& h = host_alloc_hooks();
+        if (h.alloc && bytes >= h.min_bytes) p = static_cast<T*>(h.alloc(bytes));
+        hooked = p != nullptr;
+        if (!p) p = static_cast<T*>(::operator new(bytes));
         n = count;
     }
     void reset() {
-        p.reset();
-        n = 0;
+        if (p) {
+            if (hooked) host_alloc_hooks().free(p, bytes);
+            else ::operator delete(p);
+        }
+        p = nullptr;
+        n = bytes = 0;
+        hooked = false;
     }
-    T* data() { return p.get(); }
-    const T* data() const { return p.get(); }
+    T* data() { return p; }
+    const T* data() const { return p; }
     size_t size() const { return n; }
     bool empty() const { return n == 0; }
     T& operator[](size_t i) { return p[i]; }

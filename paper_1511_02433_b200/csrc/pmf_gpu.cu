@@ -139,6 +139,62 @@ void par_memcpy(void* dst, const void* src, size_t bytes) {
     for (auto& t : ts) t.join();
 }
 
+// Page-locked host blocks for the layout arrays (HostAllocHooks, layout.hpp): the layout builder fills
+// them directly and the upload is a plain DMA (no staging memcpy).  Blocks return to this cache when a
+// layout is freed and serve the next context's layouts (pinning memory costs ~0.1-0.2 s per GB; a
+// caching host allocator as deep-learning runtimes keep).  Off with PMF_NO_ALLOC_CACHE=1;
+// pmf_release_cached_memory frees the idle blocks.
+struct PinnedPool {
+    std::mutex mu;
+    std::multimap<size_t, void*> idle;  // bytes -> block
+    std::map<uintptr_t, size_t> all;    // every block (idle or in use): start -> bytes
+    void* take(size_t bytes) {
+        std::lock_guard<std::mutex> lk(mu);
+        auto it = idle.lower_bound(bytes);
+        if (it != idle.end() && it->first <= bytes + bytes / 4) {
+            void* p = it->second;
+            idle.erase(it);
+            return p;
+        }
+        void* p = nullptr;
+        if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
+        }
+        all.emplace(reinterpret_cast<uintptr_t>(p), bytes);
+        return p;
+    }
+    void give(void* p) {
+        std::lock_guard<std::mutex> lk(mu);
+        idle.emplace(all.at(reinterpret_cast<uintptr_t>(p)), p);
+    }
+    bool contains(const void* p, size_t bytes) {
+        std::lock_guard<std::mutex> lk(mu);
+        const uintptr_t a = reinterpret_cast<uintptr_t>(p);
+        auto it = all.upper_bound(a);
+        if (it == all.begin()) return false;
+        --it;
+        return a + bytes <= it->first + it->second;
+    }
+    int64_t release_idle() {
+        std::lock_guard<std::mutex> lk(mu);
+        int64_t b = 0;
+        for (auto& kv : idle) {
+            cudaFreeHost(kv.second);
+            all.erase(reinterpret_cast<uintptr_t>(kv.second));
+            b += static_cast<int64_t>(kv.first);
+        }
+        idle.clear();
+        return b;
+    }
+};
+PinnedPool& pinned_pool() {
+    static PinnedPool* p = new PinnedPool();  // never destroyed: blocks live until process exit
+    return *p;
+}
+void* pinned_hook_alloc(size_t bytes) { return pinned_pool().take(bytes); }
+void pinned_hook_free(void* p, size_t) { pinned_pool().give(p); }
+
 double now_s();
 double g_alloc_s = 0, g_h2d_s = 0;  // PMF_VERBOSE setup breakdown (host seconds in cudaMalloc / staged_h2d)
 
@@ -148,7 +204,9 @@ void staged_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
         double t0 = now_s();
         ~Clock() { g_h2d_s += now_s() - t0; }
     } clk;
-    if (bytes < kStageMin) {
+    if (bytes < kStageMin || pinned_pool().contains(src, bytes)) {
+        // small, or already page-locked (a pooled layout array: the caller keeps it alive until the
+        // stream has been synchronised)
         CUDA_TRY(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s));
         return;
     }
@@ -406,6 +464,13 @@ void ensure_device() {
         cudaGetLastError();
         throw PmfError(PMF_RUNTIME_ERROR, "no CUDA device available (the B200 path has no CPU fallback)");
     }
+    static const bool hooks = [] {
+        if (!BlockCache::enabled()) return false;
+        host_alloc_hooks().alloc = pinned_hook_alloc;
+        host_alloc_hooks().free = pinned_hook_free;
+        return true;
+    }();
+    (void)hooks;
 }
 
 DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
@@ -1171,7 +1236,7 @@ const char* pmf_last_error(void) { return g_err.c_str(); }
 int32_t pmf_abi_version(void) { return PMF_ABI_VERSION; }
 pmf_status pmf_release_cached_memory(int64_t* released) {
     return guard([&] {
-        const int64_t b = block_cache().flush();
+        const int64_t b = block_cache().flush() + pinned_pool().release_idle();
         if (released) *released = b;
     });
 }
