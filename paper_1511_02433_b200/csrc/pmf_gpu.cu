@@ -594,15 +594,15 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     const int32_t* rmap = c->rmap.empty() ? nullptr : c->rmap.data();
     const int32_t* cmap = c->cmap.empty() ? nullptr : c->cmap.data();
     const double t_layout = now_s();
-    c->hcsr = build_sweep_layout(a->row_start, a->col_of, a->val_row, c->row_begin, c->row_end, cmap, c->ext_n,
-                                 2, smem_budget(), c->sm_count);
-    // the CSC layout is built on a host thread while the CSR layout uploads (the future's destructor
-    // waits for the builder if anything below throws)
+    // the CSC layout is built on a host thread alongside the CSR layout and its upload (the future's
+    // destructor waits for the builder if anything below throws); PMF_SETUP_SERIAL=1: after them
     static const bool serial = std::getenv("PMF_SETUP_SERIAL") != nullptr;
     auto csc_future = std::async(serial ? std::launch::deferred : std::launch::async, [&] {
         return build_sweep_layout(a->col_start, a->row_of, a->val_col, c->col_begin, c->col_end, rmap, c->ext_m, 3,
                                   smem_budget(), c->sm_count);
     });
+    c->hcsr = build_sweep_layout(a->row_start, a->col_of, a->val_row, c->row_begin, c->row_end, cmap, c->ext_n,
+                                 2, smem_budget(), c->sm_count);
     c->local_nnz_csr = a->row_start[c->row_end] - a->row_start[c->row_begin];
     c->local_nnz_csc = a->col_start[c->col_end] - a->col_start[c->col_begin];
     c->row_start_local.assign(a->row_start + c->row_begin, a->row_start + c->row_end + 1);
@@ -630,7 +630,7 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     if (std::getenv("PMF_VERBOSE"))
         std::fprintf(stderr,
                      "[pmf] ctx setup %.3f s: device init %.3f, csr layout %.3f, csr upload %.3f (csc layout "
-                     "in parallel), csc wait %.3f, csc upload %.3f, rest %.3f; process totals: cudaMalloc %.3f, "
+                     "alongside), csc wait %.3f, csc upload %.3f, rest %.3f; process totals: cudaMalloc %.3f, "
                      "staged h2d %.3f\n",
                      c->setup_seconds, t_layout - t0, t_upload - t_layout, t_csr - t_upload, t_csc - t_csr,
                      t_done - t_csc, now_s() - t_done, g_alloc_s, g_h2d_s);
