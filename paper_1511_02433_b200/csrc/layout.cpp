@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <numeric>
@@ -153,6 +154,10 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
                                int32_t out_begin, int32_t out_end, const int32_t* gmap,
                                int32_t gat_extent, int stage_arrays, int smem_budget_bytes,
                                int ctas, bool allow_idx16) {
+    static const bool verbose = std::getenv("PMF_VERBOSE") != nullptr;
+    auto clk = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
+    double tp[8] = {clk()};
+
     SweepLayout L;
     const int32_t n_out = out_end - out_begin;
     L.n_out = n_out;
@@ -185,6 +190,11 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     // panel of gather index g, tracked incrementally along an output's ascending indices
     auto count_segments = [&](int32_t pg, int32_t np, std::vector<int32_t>& seg_len) {
         seg_len.assign(static_cast<size_t>(np) * n_out, 0);
+        if (np == 1) {  // one panel: the segments are the outputs
+            for (int32_t o = 0; o < n_out; ++o)
+                seg_len[o] = static_cast<int32_t>(start[out_begin + o + 1] - start[out_begin + o]);
+            return;
+        }
         parallel_for_outputs(start, out_begin, n_out, [&](int64_t ob, int64_t oe) {
             for (int64_t o = ob; o < oe; ++o) {
                 int32_t p = 0;
@@ -269,6 +279,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     }();
     L.flat = L.smem && L.idx16 && (flat_env >= 0 ? flat_env != 0 : !L.promote_fused);
 
+    tp[1] = clk();
     // ---- 2. segment offsets (panel-major) ----------------------------------------------------
     std::vector<int64_t> seg_off(seg_len.size() + 1, 0);  // start of segment s; seg_off[S] = end
     std::vector<int64_t> seg_end(seg_len.size(), 0);
@@ -289,6 +300,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     L.avg_segment = nonempty ? static_cast<double>(nnz_side) / nonempty : 0.0;
     if (L.n_entries >= (int64_t(1) << 32)) throw std::length_error("too many entries for 32-bit units");
 
+    tp[2] = clk();
     // ---- 3. fill entries (padding of each segment written by its owner thread) -----------------
     if (L.idx16) L.idx16v.alloc(L.n_entries);
     else L.idx32v.alloc(L.n_entries);
@@ -333,6 +345,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
         }
     });
 
+    tp[3] = clk();
     // ---- 4. units ----------------------------------------------------------------------------
     std::vector<int32_t> cnt(n_out, 0), ovf(n_out, 0);
     std::vector<uint8_t> chunk0;  // unit is the first chunk of its segment
@@ -386,6 +399,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
         }
     }
 
+    tp[4] = clk();
     // ---- 5. per-CTA pieces: contiguous unit ranges of equal cost, split at panel changes -----
     const int64_t nu = static_cast<int64_t>(L.units.size());
     const UnitCost cm = unit_cost_model();
@@ -481,6 +495,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
         }
     }
 
+    tp[5] = clk();
     // ---- 6. sub-panel split points of the residual pass (entries are ascending within a unit) ---
     if (L.rmw_sub > 1) {
         const int S = L.rmw_sub;
@@ -500,6 +515,12 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
             }
         });
     }
+    if (verbose)
+        std::fprintf(stderr,
+                     "[pmf] layout (%d outputs, %lld entries): panels %.3f, offsets %.3f, fill %.3f, units %.3f, "
+                     "pieces %.3f, rest %.3f s\n",
+                     static_cast<int>(L.n_out), static_cast<long long>(L.n_entries), tp[1] - tp[0], tp[2] - tp[1],
+                     tp[3] - tp[2], tp[4] - tp[3], tp[5] - tp[4], clk() - tp[5]);
     return L;
 }
 
