@@ -349,6 +349,15 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     // ---- 4. units ----------------------------------------------------------------------------
     std::vector<int32_t> cnt(n_out, 0), ovf(n_out, 0);
     std::vector<uint8_t> chunk0;  // unit is the first chunk of its segment
+    {
+        size_t n_units = 0;
+        for (size_t s = 0; s < seg_len.size(); ++s)
+            if (seg_len[s]) n_units += static_cast<size_t>((seg_end[s] - seg_off[s] + kUnitMax - 1) / kUnitMax);
+        L.units.reserve(n_units);
+        L.unit_panel.reserve(n_units);
+        L.unit_real.reserve(n_units);
+        chunk0.reserve(n_units);
+    }
     for (int32_t p = 0; p < np; ++p)
         for (int32_t o = 0; o < n_out; ++o) {
             const size_t s = static_cast<size_t>(p) * n_out + o;
@@ -417,12 +426,22 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
                      cm.per_unit[c] + (u > 0 && L.unit_panel[u] != L.unit_panel[u - 1] ? cm.per_piece : 0);
     }
     L.piece_start.assign(ctas + 1, 0);
-    int64_t ub = 0;
+    std::vector<int64_t> cta_ub(ctas + 1, 0);
     for (int c = 0; c < ctas; ++c) {
         const int64_t target = pre[nu] * (c + 1) / ctas;
         int64_t ue = std::lower_bound(pre.begin(), pre.end(), target) - pre.begin();
-        ue = std::max(ub, std::min(ue, nu));
+        ue = std::max(cta_ub[c], std::min(ue, nu));
         if (c == ctas - 1) ue = nu;
+        cta_ub[c + 1] = ue;
+    }
+    // the CTAs' unit ranges are disjoint: their pieces are formed on parallel threads (chunk indices
+    // are per CTA here and rebased when the lists are joined)
+    std::vector<std::vector<Piece>> cta_pieces(ctas);
+    std::vector<std::vector<FlatChunk>> cta_chunks(ctas);
+    auto form = [&](int c) {
+        std::vector<Piece>& lpieces = cta_pieces[c];
+        std::vector<FlatChunk>& lchunks = cta_chunks[c];
+        const int64_t ub = cta_ub[c], ue = cta_ub[c + 1];
         for (int64_t u = ub; u < ue;) {
             int64_t v = u;
             while (v < ue && L.unit_panel[v] == L.unit_panel[u]) ++v;
@@ -463,7 +482,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
             Piece pz{L.unit_panel[u], static_cast<int32_t>(u), static_cast<int32_t>(um),
                      static_cast<int32_t>(us), static_cast<int32_t>(v), {0, 0, 0}};
             if (L.flat) {  // chunks of whole units: <= kFlatChunkVectors vectors (one unit if longer), <= kFlatChunkUnits units
-                pz.pad[0] = static_cast<int32_t>(L.chunks.size());
+                pz.pad[0] = static_cast<int32_t>(lchunks.size());
                 for (int64_t x = u; x < v;) {
                     const int32_t v0 = static_cast<int32_t>(L.units[x].e0 / 4);
                     int64_t y = x;
@@ -474,16 +493,35 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
                         v1 = static_cast<int32_t>((static_cast<int64_t>(L.units[y].e0) + L.units[y].len) / 4);
                         ++y;
                     }
-                    L.chunks.push_back(FlatChunk{static_cast<int32_t>(x), v0, v1, static_cast<int32_t>(y)});
+                    lchunks.push_back(FlatChunk{static_cast<int32_t>(x), v0, v1, static_cast<int32_t>(y)});
                     x = y;
                 }
-                pz.pad[1] = static_cast<int32_t>(L.chunks.size());
+                pz.pad[1] = static_cast<int32_t>(lchunks.size());
             }
-            L.pieces.push_back(pz);
+            lpieces.push_back(pz);
             u = v;
         }
+    };
+    {
+        const int T = std::max(1, std::min<int>(ctas, static_cast<int>(std::thread::hardware_concurrency())));
+        std::vector<std::thread> ts;
+        for (int t = 0; t < T; ++t)
+            ts.emplace_back([&, t] {
+                for (int c = t; c < ctas; c += T) form(c);
+            });
+        for (auto& t : ts) t.join();
+    }
+    for (int c = 0; c < ctas; ++c) {
+        const int32_t base = static_cast<int32_t>(L.chunks.size());
+        for (Piece pz : cta_pieces[c]) {
+            if (L.flat) {
+                pz.pad[0] += base;
+                pz.pad[1] += base;
+            }
+            L.pieces.push_back(pz);
+        }
+        L.chunks.insert(L.chunks.end(), cta_chunks[c].begin(), cta_chunks[c].end());
         L.piece_start[c + 1] = static_cast<int32_t>(L.pieces.size());
-        ub = ue;
     }
 
     if (L.flat) {
