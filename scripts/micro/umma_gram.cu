@@ -4,10 +4,12 @@
 // Verified on the B200 with both operands K-major, no swizzle (core matrices of 8 features x 16 B;
 // UG_FLAG=4): max relative error 5.6e-2 on near-zero entries, absolute 4e-3 (TF32 operands), and the
 // M = 64 accumulator layout row m -> TMEM lane (m % 16) + 32 (m / 16).  The MN-major SWIZZLE_128B
-// variant (UG_FLAG=0, the layout TMA gather4 would write directly) reads zero operands: its
-// descriptor (LBO = MN-atom stride, SBO = 8-row K-group stride, as in cute's make_umma_desc) is not
-// right yet.  UG_FLAG bits: 1 = seed D with 7 and accumulate (checks what the MMA wrote), 2 = print
-// the smem / TMEM bases, 4 = K-major layout.  UG_DUMP=1 prints rows.
+// variant (UG_FLAG=0, the layout TMA gather4 would write directly) reads zero operands, with LBO / SBO
+// either way round (UG_FLAG=8), and so does MN-major without swizzle (UG_FLAG=16): with these
+// instruction-descriptor bits (a/b major = 1, bits 15/16) MN-major TF32 operands come back as zeros,
+// so the product path will transpose the gathered rows into K-major core matrices.  UG_FLAG bits:
+// 1 = seed D with 7 and accumulate (shows what the MMA added), 2 = print the smem / TMEM bases,
+// 4 = K-major layout, 8 = swapped LBO / SBO, 16 = MN-major no swizzle.  UG_DUMP=1 prints rows.
 //   nvcc -O2 -gencode arch=compute_100a,code=sm_100a -o umma_gram umma_gram.cu && UG_FLAG=4 ./umma_gram
 #include <cuda_runtime.h>
 
@@ -40,6 +42,12 @@ __host__ __device__ inline uint32_t kmajor_offset(int e, int f) {
     return (f % 8) * 16 + (f / 8) * 1024 + (e % 4) * 4 + (e / 4) * 128;
 }
 
+// MN-major, no swizzle: core matrices of 4 features (16 B) x 8 entries (128 B contiguous), the next
+// 4 features SBO = 128 B on, the next 8 entries LBO = 2 KB on
+__host__ __device__ inline uint32_t mn_inter_offset(int e, int f) {
+    return (f % 4) * 4 + (e % 8) * 16 + (f / 4) * 128 + (e / 8) * 2048;
+}
+
 __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
     uint64_t d = 0;
     d |= static_cast<uint64_t>((saddr >> 4) & 0x3fff);
@@ -59,7 +67,9 @@ __global__ void __launch_bounds__(128, 1) umma_gram(const float* __restrict__ X,
     // stage X (K x F, row-major in global) into the swizzled MN-major layout
     for (int i = tid; i < K * F; i += blockDim.x) {
         const int e = i / F, f = i % F;
-        *reinterpret_cast<float*>(smem + ((getenv_flag & 4) ? kmajor_offset(e, f) : sw128_offset(e, f))) = X[i];
+        *reinterpret_cast<float*>(smem + ((getenv_flag & 4)    ? kmajor_offset(e, f)
+                                          : (getenv_flag & 16) ? mn_inter_offset(e, f)
+                                                               : sw128_offset(e, f))) = X[i];
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     if (tid == 0) {
@@ -93,7 +103,11 @@ __global__ void __launch_bounds__(128, 1) umma_gram(const float* __restrict__ X,
         const uint32_t base = smem_u32(smem);
         for (int s = 0; s < K / 8; ++s) {
             const bool km = getenv_flag & 4;
-            const uint64_t ad = km ? make_desc(base + s * 256, 128, 1024, 0) : make_desc(base + s * sbo, lbo, sbo, 2);
+            const bool swap = getenv_flag & 8;  // MN-major: try LBO / SBO the other way round
+            const uint64_t ad = km                  ? make_desc(base + s * 256, 128, 1024, 0)
+                                : (getenv_flag & 16) ? make_desc(base + s * 2048, 2048, 128, 0)
+                                : swap ? make_desc(base + s * sbo, sbo, lbo, 2)
+                                       : make_desc(base + s * sbo, lbo, sbo, 2);
             const uint64_t bd = ad;
             const uint32_t acc = (s > 0 || (getenv_flag & 1)) ? 1u : 0u;
             asm volatile(
