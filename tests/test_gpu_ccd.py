@@ -274,3 +274,27 @@ def test_release_cached_memory(pmf, ml100k):
     assert pmf.release_cached_memory() == 0
     m2, _ = pmf.ccdpp_train(cfg, A, probe)
     assert m1 == m2
+
+
+def test_alloc_cache_off_same_model(pmf, tmp_path):
+    """PMF_NO_ALLOC_CACHE=1 (plain cudaMalloc, pageable layout arrays through the staging buffers) trains
+    the same model bit for bit as the cached device blocks + page-locked layout blocks (5M ratings: the
+    layout arrays are above the 16 MB page-locked threshold)."""
+    import subprocess
+    import sys
+    m, n = 30000, 2000
+    train, _ = pmf.synth_ratings(m, n, 3, 5_000_000, 1000, 11)
+    A = pmf.RatingsMatrix.from_triplets(train, m, n)
+    cfg = pmf.CcdConfig(k=4, lam=0.05, outer_iters=2, inner_iters=3, seed=2)
+    m1, _ = pmf.ccdpp_train(cfg, A)
+    np.save(tmp_path / "train.npy", train)
+    code = (
+        "import sys, numpy as np; sys.path.insert(0, sys.argv[1]); import paper_1511_02433_b200 as P\n"
+        "t = np.load(sys.argv[2]); A = P.RatingsMatrix.from_triplets(t, 30000, 2000)\n"
+        "m, _ = P.ccdpp_train(P.CcdConfig(k=4, lam=0.05, outer_iters=2, inner_iters=3, seed=2), A)\n"
+        "np.save(sys.argv[3], m.w); np.save(sys.argv[4], m.h)\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, PMF_NO_ALLOC_CACHE="1")
+    subprocess.run([sys.executable, "-c", code, root, str(tmp_path / "train.npy"), str(tmp_path / "w.npy"),
+                    str(tmp_path / "h.npy")], check=True, env=env, timeout=300)
+    assert np.array_equal(np.load(tmp_path / "w.npy"), m1.w) and np.array_equal(np.load(tmp_path / "h.npy"), m1.h)
