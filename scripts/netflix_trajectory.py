@@ -2,7 +2,8 @@
 of the B200 path and of the reference (parmf compiled from its headers, oracle/_ref, all host threads) on
 the same synthetic Netflix-shape data (bench.make_data: 480,189 x 17,770, 99M ratings), CCD++ (k = 40,
 T = 15) and ALS (k = 40), plus the relative Frobenius distance of the factors.  Writes
-gpurun_out/netflix_trajectory.json.  OUTER_CCD / OUTER_ALS set the iteration counts (3 / 2)."""
+gpurun_out/<config>_trajectory.json.  OUTER_CCD / OUTER_ALS set the iteration counts (3 / 2);
+CONFIG=yahoo-ccdpp runs the Yahoo-Music shape (k = 100, CCD++ only: the ALS kernels take k <= 64)."""
 import json
 import os
 import sys
@@ -27,24 +28,25 @@ def frob(a, b):
 def main():
     oc = int(os.environ.get("OUTER_CCD", "3"))
     oa = int(os.environ.get("OUTER_ALS", "2"))
-    train, probe, A = bench.make_data("netflix-ccdpp")
-    m, n = 480189, 17770
+    cfg = os.environ.get("CONFIG", "netflix-ccdpp")
+    m, n, _, _, k, *_ = bench.CONFIGS[cfg]
+    train, probe, A = bench.make_data(cfg)
     ref = Reference()
     workers = os.cpu_count() or 1
     RA = RefMatrix(ref, train, m, n, "_f32")
-    out = {"workers": workers, "config": "netflix-shape synthetic, k=40, lambda=0.05, seed 1"}
-    for algo in ("ccdpp", "als"):
+    out = {"workers": workers, "config": f"{cfg} synthetic, k={k}, lambda=0.05, seed 1"}
+    for algo in ("ccdpp", "als") if k <= 64 else ("ccdpp",):
         t0 = time.time()
         if algo == "ccdpp":
-            model, rep = P.ccdpp_train(P.CcdConfig(k=40, lam=0.05, outer_iters=oc, inner_iters=15, seed=1), A, probe)
+            model, rep = P.ccdpp_train(P.CcdConfig(k=k, lam=0.05, outer_iters=oc, inner_iters=15, seed=1), A, probe)
         else:
-            model, rep = P.als_train(P.AlsConfig(k=40, lam=0.05, outer_iters=oa, seed=1), A, probe)
+            model, rep = P.als_train(P.AlsConfig(k=k, lam=0.05, outer_iters=oa, seed=1), A, probe)
         t_gpu = time.time() - t0
         t0 = time.time()
         if algo == "ccdpp":
-            W, H, rows = RA.ccdpp_train(40, 0.05, oc, 15, 1, probe, workers)
+            W, H, rows = RA.ccdpp_train(k, 0.05, oc, 15, 1, probe, workers)
         else:
-            W, H, rows = RA.als_train(40, 0.05, oa, 1, probe, workers)
+            W, H, rows = RA.als_train(k, 0.05, oa, 1, probe, workers)
         t_ref = time.time() - t0
         its = []
         for r, g in zip(rep.rows, rows):
@@ -60,7 +62,7 @@ def main():
         print(f"{algo}: factors rel Frobenius W {out[algo]['frob_rel_W']:.2e} H {out[algo]['frob_rel_H']:.2e}; "
               f"wall GPU {t_gpu:.1f} s (incl. setup) vs reference {t_ref:.1f} s", flush=True)
     os.makedirs("gpurun_out", exist_ok=True)
-    with open("gpurun_out/netflix_trajectory.json", "w") as fh:
+    with open(f"gpurun_out/{cfg.split('-')[0]}_trajectory.json", "w") as fh:
         json.dump(out, fh, indent=1)
 
 
