@@ -1,8 +1,8 @@
 """Netflix-shape parity against the reference itself: per-iteration objective, probe RMSE and train RMSE
 of the B200 path and of the reference (parmf compiled from its headers, oracle/_ref, all host threads) on
 the same synthetic Netflix-shape data (bench.make_data: 480,189 x 17,770, 99M ratings), CCD++ (k = 40,
-T = 15) and ALS (k = 40), plus the relative Frobenius distance of the factors.  Writes
-gpurun_out/<config>_trajectory.json.  OUTER_CCD / OUTER_ALS set the iteration counts (3 / 2);
+T = 15), ALS and item/user-wise CCD (k = 40), plus the relative Frobenius distance of the factors.  Writes
+gpurun_out/<config>_trajectory.json.  OUTER_CCD / OUTER_ALS / OUTER_CCDW set the iteration counts (3 / 2 / 2), ALGOS the algorithms;
 CONFIG=yahoo-ccdpp runs the Yahoo-Music shape (k = 100, CCD++ only: the ALS kernels take k <= 64)."""
 import json
 import os
@@ -35,18 +35,24 @@ def main():
     workers = os.cpu_count() or 1
     RA = RefMatrix(ref, train, m, n, "_f32")
     out = {"workers": workers, "config": f"{cfg} synthetic, k={k}, lambda=0.05, seed 1"}
-    for algo in ("ccdpp", "als") if k <= 64 else ("ccdpp",):
+    ow = int(os.environ.get("OUTER_CCDW", "2"))
+    algos = os.environ.get("ALGOS", "ccdpp,als,ccd").split(",")
+    for algo in [a for a in algos if a == "ccdpp" or k <= 64]:
         t0 = time.time()
         if algo == "ccdpp":
             model, rep = P.ccdpp_train(P.CcdConfig(k=k, lam=0.05, outer_iters=oc, inner_iters=15, seed=1), A, probe)
-        else:
+        elif algo == "als":
             model, rep = P.als_train(P.AlsConfig(k=k, lam=0.05, outer_iters=oa, seed=1), A, probe)
+        else:  # item/user-wise CCD (ccd.hpp:310-344)
+            model, rep = P.ccd_train(P.CcdConfig(k=k, lam=0.05, outer_iters=ow, inner_iters=1, seed=1), A, probe)
         t_gpu = time.time() - t0
         t0 = time.time()
         if algo == "ccdpp":
             W, H, rows = RA.ccdpp_train(k, 0.05, oc, 15, 1, probe, workers)
-        else:
+        elif algo == "als":
             W, H, rows = RA.als_train(k, 0.05, oa, 1, probe, workers)
+        else:
+            W, H, rows = RA.ccd_train(k, 0.05, ow, 1, probe)
         t_ref = time.time() - t0
         its = []
         for r, g in zip(rep.rows, rows):
