@@ -667,13 +667,14 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
 
 // Fixed-order combination of the partial sums of outputs with several (or zero) units: the dense
 // slots p * n_out + o over the panels in order, then the output's overflow slots.  Outputs
-// [0, n_big) have many slots: a warp each (lane-strided, xor tree); the rest 4 lanes each (every
-// 4th slot per lane, then a 2-level xor tree; the dense slots of adjacent outputs are adjacent).
+// [0, n_big) have many slots: a warp each (lane-strided, xor tree); the rest 1 lane each, or 4 lanes
+// each with >= 24 panels (every 4th slot per lane, then a 2-level xor tree); the dense slots of
+// adjacent outputs are adjacent.
 constexpr int kFinalizeThreads = 256;
 __global__ void finalize_kernel(const int32_t* __restrict__ mo_out, const int32_t* __restrict__ mo_start,
                                 int32_t n_mo, int32_t n_big, int32_t big_blocks, const float2* __restrict__ partial,
                                 int32_t n_panels, int32_t n_out, int64_t n_dense, float* __restrict__ out,
-                                int32_t out_off, float lambda) {
+                                int32_t out_off, float lambda, int lpo) {
     const float2* ovf = partial + n_dense;
     if (static_cast<int32_t>(blockIdx.x) < big_blocks) {
         const int lane = threadIdx.x & 31;
@@ -705,10 +706,11 @@ __global__ void finalize_kernel(const int32_t* __restrict__ mo_out, const int32_
         }
         return;
     }
-    // the rest: 4 lanes per output, each summing every 4th slot in order, then a fixed 2-level tree
-    // (a few dependent loads per lane instead of one chain of all the output's slots)
-    const int64_t q = n_big + (static_cast<int64_t>(blockIdx.x - big_blocks) * blockDim.x + threadIdx.x) / 4;
-    const int sub = threadIdx.x & 3;
+    // the rest: lpo (1 or 4) lanes per output, each summing every lpo-th slot in order, then a fixed
+    // 2-level tree (with many panels: a few dependent loads per lane instead of one long chain)
+    const int64_t q =
+        n_big + (static_cast<int64_t>(blockIdx.x - big_blocks) * blockDim.x + threadIdx.x) / lpo;
+    const int sub = lpo == 4 ? (threadIdx.x & 3) : 0;
     const bool valid = q < n_mo;
     float num = 0.f, den = 0.f;
     int o = 0;
@@ -716,21 +718,23 @@ __global__ void finalize_kernel(const int32_t* __restrict__ mo_out, const int32_
         o = mo_out[q];
         const int s0 = mo_start[q], s1 = mo_start[q + 1];
 #pragma unroll 4
-        for (int p = sub; p < n_panels; p += 4) {
+        for (int p = sub; p < n_panels; p += lpo) {
             const float2 v = partial[static_cast<int64_t>(p) * n_out + o];
             num += v.x;
             den += v.y;
         }
-        for (int s = s0 + sub; s < s1; s += 4) {
+        for (int s = s0 + sub; s < s1; s += lpo) {
             const float2 v = ovf[s];
             num += v.x;
             den += v.y;
         }
     }
-    num += __shfl_xor_sync(0xffffffffu, num, 1);
-    den += __shfl_xor_sync(0xffffffffu, den, 1);
-    num += __shfl_xor_sync(0xffffffffu, num, 2);
-    den += __shfl_xor_sync(0xffffffffu, den, 2);
+    if (lpo == 4) {
+        num += __shfl_xor_sync(0xffffffffu, num, 1);
+        den += __shfl_xor_sync(0xffffffffu, den, 1);
+        num += __shfl_xor_sync(0xffffffffu, num, 2);
+        den += __shfl_xor_sync(0xffffffffu, den, 2);
+    }
     if (valid && sub == 0) {
         const float dt = __fadd_rn(lambda, den);
         out[out_off + o] = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
@@ -858,11 +862,12 @@ int launch_finalize(const DevSweep& L, const SweepOperands& op, cudaStream_t str
     if (L.n_mo <= 0) return 0;
     const int big_blocks = static_cast<int>(std::min<int64_t>(
         (static_cast<int64_t>(L.n_mo_big) * 32 + kFinalizeThreads - 1) / kFinalizeThreads, 1184));
-    const int small_blocks = static_cast<int>((4 * static_cast<int64_t>(L.n_mo - L.n_mo_big) + kFinalizeThreads - 1) /
+    const int lpo = L.n_dense && L.n_panels >= 24 ? 4 : 1;  // lanes per output (Netflix CSC: 26 panels)
+    const int small_blocks = static_cast<int>((lpo * static_cast<int64_t>(L.n_mo - L.n_mo_big) + kFinalizeThreads - 1) /
                                               kFinalizeThreads);
     finalize_kernel<<<big_blocks + small_blocks, kFinalizeThreads, 0, stream>>>(
         L.mo_out, L.mo_start, L.n_mo, L.n_mo_big, big_blocks, L.partial, L.n_dense ? L.n_panels : 0, L.n_out,
-        L.n_dense, op.out, op.out_off, op.lambda);
+        L.n_dense, op.out, op.out_off, op.lambda, lpo);
     return 1;
 }
 
