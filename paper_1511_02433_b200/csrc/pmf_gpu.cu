@@ -890,14 +890,19 @@ struct AlsHost {
     AlsLayout csr, csc;
 };
 
-constexpr int kAlsChunk = 4096;
+// entries per ALS work unit (PMF_ALS_CHUNK): longer rows / columns split into partial grams.  Netflix
+// k = 40: 4096 -> 16.95 ms, 16384 -> 16.69 ms, 65536 -> 19.6 ms per iteration (fewer partials vs balance)
+int als_chunk() {
+    static const int c = std::getenv("PMF_ALS_CHUNK") ? std::max(32, std::atoi(std::getenv("PMF_ALS_CHUNK"))) : 16384;
+    return c;
+}
 
 void build_als(Ctx& c, const pmf_matrix_view* a) {
     if (c.als_built) return;
     const int32_t* rmap = c.rmap.empty() ? nullptr : c.rmap.data();
     const int32_t* cmap = c.cmap.empty() ? nullptr : c.cmap.data();
-    AlsLayout lc = build_als_layout(a->row_start, a->col_of, a->val_row, c.row_begin, c.row_end, cmap, kAlsChunk);
-    AlsLayout lr = build_als_layout(a->col_start, a->row_of, a->val_col, c.col_begin, c.col_end, rmap, kAlsChunk);
+    AlsLayout lc = build_als_layout(a->row_start, a->col_of, a->val_row, c.row_begin, c.row_end, cmap, als_chunk());
+    AlsLayout lr = build_als_layout(a->col_start, a->row_of, a->val_col, c.col_begin, c.col_end, rmap, als_chunk());
     c.als_csr = upload_als(c, lc, 0);
     c.als_csc = upload_als(c, lr, 0);
     c.d_counter = c.als_mem.alloc<int>(4);

@@ -59,12 +59,12 @@ def test_solve_rows_vs_oracle(pmf, oracle, k):
 
 
 def test_long_columns_use_chunked_partials(pmf, oracle):
-    """Columns longer than the 4096-entry chunk go through the fixed-order partial reduction."""
-    m, n = 20000, 40
-    t = oracle.synth_ratings(m, n, 3, 200000, 5)
+    """Columns longer than the 16384-entry chunk go through the fixed-order partial reduction."""
+    m, n = 100000, 20
+    t = oracle.synth_ratings(m, n, 3, 600000, 5)
     A = pmf.RatingsMatrix.from_triplets(t, m, n)
     O = oracle.from_triplets(t, m, n)
-    assert np.diff(A.col_start).max() > 4096
+    assert np.diff(A.col_start).max() > 16384
     rng = np.random.default_rng(0)
     w = (rng.uniform(0, 1, (m, 10)) / math.sqrt(10)).astype(np.float32)
     h_gpu = pmf.solve_item_rows(A, w, 10, 0.05)
