@@ -890,10 +890,15 @@ struct AlsHost {
     AlsLayout csr, csc;
 };
 
-// entries per ALS work unit (PMF_ALS_CHUNK): longer rows / columns split into partial grams.  Netflix
-// k = 40: 4096 -> 16.95 ms, 16384 -> 16.69 ms, 65536 -> 19.6 ms per iteration (fewer partials vs balance)
-int als_chunk() {
-    static const int c = std::getenv("PMF_ALS_CHUNK") ? std::max(32, std::atoi(std::getenv("PMF_ALS_CHUNK"))) : 16384;
+// Entries per ALS / CCD gram work unit (longer rows / columns split into partial grams).  Large
+// enough that few outputs need partials, small enough that the longest units do not leave a tail:
+// the power of two nearest nnz / (2 x resident warps), in [1024, 16384] (Netflix: 16384 -- 4096 gave
+// 16.95 ms, 16384 16.69 ms, 65536 19.6 ms per ALS iteration; ML-10M: 2048).  PMF_ALS_CHUNK overrides.
+int als_chunk(int64_t nnz, int sm_count) {
+    if (const char* e = std::getenv("PMF_ALS_CHUNK")) return std::max(32, std::atoi(e));
+    const int64_t target = nnz / (2 * 20 * static_cast<int64_t>(std::max(sm_count, 1)));
+    int c = 1024;
+    while (c < 16384 && 2 * c <= target) c *= 2;
     return c;
 }
 
@@ -901,8 +906,9 @@ void build_als(Ctx& c, const pmf_matrix_view* a) {
     if (c.als_built) return;
     const int32_t* rmap = c.rmap.empty() ? nullptr : c.rmap.data();
     const int32_t* cmap = c.cmap.empty() ? nullptr : c.cmap.data();
-    AlsLayout lc = build_als_layout(a->row_start, a->col_of, a->val_row, c.row_begin, c.row_end, cmap, als_chunk());
-    AlsLayout lr = build_als_layout(a->col_start, a->row_of, a->val_col, c.col_begin, c.col_end, rmap, als_chunk());
+    const int chunk = als_chunk(c.nnz, c.sm_count);
+    AlsLayout lc = build_als_layout(a->row_start, a->col_of, a->val_row, c.row_begin, c.row_end, cmap, chunk);
+    AlsLayout lr = build_als_layout(a->col_start, a->row_of, a->val_col, c.col_begin, c.col_end, rmap, chunk);
     c.als_csr = upload_als(c, lc, 0);
     c.als_csc = upload_als(c, lr, 0);
     c.d_counter = c.als_mem.alloc<int>(4);
@@ -994,10 +1000,14 @@ void ccdw_begin(Ctx& c, const pmf_ccd_config* cfg) {
     c.ccdw_mem.free_all();
     c.k = cfg->k;
     c.lambda = cfg->lambda;
-    // k <= 40: each row's (column's) coordinate sweep is one Gauss-Seidel sweep on its normal
-    // equations, whose gram and right-hand side come off the ALS tensor-core gram kernel; otherwise
-    // (or PMF_CCD_RESIDUAL) the residual-based warp-per-row / CTA-per-column kernels
-    c.ccdw_gram = als_gram_gs_supported(c.k) && std::getenv("PMF_CCD_RESIDUAL") == nullptr;
+    // Default: the residual form (warp per row / CTA per column), which updates a float residual
+    // entry by entry as the reference does and tracks its trajectory to ~3e-6 over 5 Netflix epochs.
+    // PMF_CCD_GRAM=1 (k <= 40): each row's (column's) coordinate sweep as one Gauss-Seidel sweep on
+    // its normal equations, gram and right-hand side from the ALS tensor-core kernel, no residual --
+    // 10x faster, but it does not carry the reference's residual rounding, and the objectives drift
+    // apart (1e-4 relative after 3-4 Netflix epochs).
+    const char* gram_env = std::getenv("PMF_CCD_GRAM");
+    c.ccdw_gram = als_gram_gs_supported(c.k) && gram_env && std::atoi(gram_env) != 0;
     if (c.ccdw_gram) {
         c.W = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_m + 1) * c.k);  // W = 0 (ccd.hpp:323)
         c.H = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_n + 1) * c.k);

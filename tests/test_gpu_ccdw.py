@@ -1,8 +1,8 @@
 """GPU item/user-wise CCD (ccd.hpp:52-125, ccd_train :310-344) against the oracle
 (pinned to the reference in test_ccd_oracle.py): per-iteration objective, train and probe RMSE within
-1e-4 relative, factors within 1e-3 relative Frobenius (k <= 40: each coordinate sweep is a Gauss-Seidel
-sweep on the row's normal equations with a tensor-core gram; k > 40: warp / CTA residual sweeps; the
-reference's sums are sequential), objective non-increasing, edge cases, both paths."""
+1e-4 relative, factors within 1e-3 relative Frobenius (default: warp / CTA residual sweeps; PMF_CCD_GRAM=1,
+k <= 40: each coordinate sweep as a Gauss-Seidel sweep on the row's normal equations with a tensor-core
+gram; the reference's sums are sequential), objective non-increasing, edge cases, both paths."""
 import numpy as np
 import pytest
 
@@ -60,15 +60,15 @@ def test_ccd_long_rows_vs_oracle(pmf, oracle):
 
 
 def test_ccd_paths_vs_oracle(pmf, oracle, ml100k, monkeypatch):
-    # k <= 40 runs the gram + Gauss-Seidel path; k > 40 (or PMF_CCD_RESIDUAL) the residual kernels
+    # default: the residual kernels; PMF_CCD_GRAM=1 (k <= 40): gram + Gauss-Seidel; k > 40 always residual
     train, probe = ml100k
     A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
     O = oracle.from_triplets(train, 943, 1682)
-    for k, residual in ((12, True), (44, False)):
-        if residual:
-            monkeypatch.setenv("PMF_CCD_RESIDUAL", "1")
+    for k, gram in ((12, True), (12, False), (44, True)):
+        if gram:
+            monkeypatch.setenv("PMF_CCD_GRAM", "1")
         else:
-            monkeypatch.delenv("PMF_CCD_RESIDUAL", raising=False)
+            monkeypatch.delenv("PMF_CCD_GRAM", raising=False)
         model, rep = pmf.ccd_train(pmf.CcdConfig(k=k, lam=0.1, outer_iters=2, inner_iters=1, seed=3), A, probe)
         W, H, rows = oracle.ccd_train(O, k, 0.1, 2, 3, probe)
         for r, g in zip(rep.rows, rows):
