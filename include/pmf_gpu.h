@@ -57,7 +57,8 @@ typedef struct pmf_matrix_view {
     const float* val_col;     /* nnz */
 } pmf_matrix_view;
 
-/* CcdConfig (ccd.hpp:33-50); `workers` becomes num_gpus (1 = this process's device). */
+/* CcdConfig (ccd.hpp:33-50); `workers` becomes num_gpus (1 = this process's device; N > 1 = a
+ * device group of N ranks, see pmf_ctx_create_group; must be >= 1 like workers, ccd.hpp:43-49). */
 typedef struct pmf_ccd_config {
     int32_t k;
     float lambda;
@@ -277,6 +278,15 @@ pmf_status pmf_nccl_unique_id(uint8_t* out128);
  * are all-gathered over NCCL after every sweep / half-step. */
 pmf_status pmf_ctx_create_dist(const pmf_matrix_view* a, int32_t device, int32_t rank,
                                int32_t world, const uint8_t* nccl_id128, pmf_ctx** out);
+/* One process driving a device group of num_gpus ranks with the same row / column block plan: rank
+ * r on devices[r] (NULL: device r mod pmf_device_count(), so ranks may share a device).  The
+ * all-gathers are device-to-device copies between the ranks' replicated vectors, ordered by
+ * events; a group whose ranks share one device runs each outer iteration as one CUDA graph.  The
+ * returned handle drives every rank through the pmf_ctx_* calls (model / metrics as one context).
+ * The whole-call entry points use this for config num_gpus > 1 (the reference's `workers`,
+ * ccd.hpp:39, als.hpp:30). */
+pmf_status pmf_ctx_create_group(const pmf_matrix_view* a, int32_t num_gpus, const int32_t* devices,
+                                pmf_ctx** out);
 
 #ifdef __cplusplus
 }

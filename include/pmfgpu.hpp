@@ -57,13 +57,13 @@ inline const pmf_triplet* probe_ptr(std::span<const parmf::Triplet<float>> probe
 }
 
 namespace detail {
-inline parmf::TrainReport report_of(const char* alg, int k, double lambda, int outer, int inner,
+inline parmf::TrainReport report_of(const char* alg, int k, double lambda, int outer, int inner, int workers,
                                     std::uint64_t seed, const parmf::RatingsMatrix<float>& a,
                                     const std::vector<pmf_iter_row>& rows, const pmf_train_totals& tot) {
     parmf::TrainReport r;
     r.algorithm = alg;
     r.precision = "single";
-    r.workers = 1;
+    r.workers = workers;
     r.k = k;
     r.lambda = lambda;
     r.outer_iters = outer;
@@ -88,7 +88,9 @@ inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> ccdpp_train(
     const parmf::CcdConfig<float>& config, const parmf::RatingsMatrix<float>& a,
     parmf::span_arg<const parmf::Triplet<float>> probe) {
     config.validate();
-    const pmf_ccd_config c{config.k, config.lambda, config.outer_iters, config.inner_iters, config.seed, 1, 0};
+    // workers (ccd.hpp:39) -> GPUs: a device group of `workers` ranks (pmf_ctx_create_group)
+    const pmf_ccd_config c{config.k, config.lambda, config.outer_iters, config.inner_iters, config.seed,
+                           config.workers, 0};
     const pmf_matrix_view v = view_of(a);
     parmf::FactorModel<float> model(a.rows(), a.cols(), config.k);
     std::vector<pmf_iter_row> rows(static_cast<size_t>(config.outer_iters));
@@ -98,7 +100,8 @@ inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> ccdpp_train(
     if (probe.empty())
         for (auto& r : rows) r.rmse = std::numeric_limits<double>::quiet_NaN();
     return {std::move(model), detail::report_of("ccdpp", config.k, static_cast<double>(config.lambda),
-                                                config.outer_iters, config.inner_iters, config.seed, a, rows, tot)};
+                                                config.outer_iters, config.inner_iters, config.workers, config.seed,
+                                                a, rows, tot)};
 }
 
 // ccd.hpp:310-344 (item/user-wise CCD; one device, inner_iters ignored like the reference)
@@ -115,9 +118,8 @@ inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> ccd_train(
                         model.h().data(), rows.data(), &tot));
     if (probe.empty())
         for (auto& r : rows) r.rmse = std::numeric_limits<double>::quiet_NaN();
-    auto rep = detail::report_of("ccd", config.k, static_cast<double>(config.lambda), config.outer_iters, 1,
+    auto rep = detail::report_of("ccd", config.k, static_cast<double>(config.lambda), config.outer_iters, 1, 1,
                                  config.seed, a, rows, tot);
-    rep.workers = 1;
     return {std::move(model), std::move(rep)};
 }
 
@@ -126,7 +128,7 @@ inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> als_train(
     const parmf::AlsConfig<float>& config, const parmf::RatingsMatrix<float>& a,
     parmf::span_arg<const parmf::Triplet<float>> probe) {
     config.validate();
-    const pmf_als_config c{config.k, config.lambda, config.outer_iters, config.seed, 1, 0};
+    const pmf_als_config c{config.k, config.lambda, config.outer_iters, config.seed, config.workers, 0};  // als.hpp:30
     const pmf_matrix_view v = view_of(a);
     parmf::FactorModel<float> model(a.rows(), a.cols(), config.k);
     std::vector<pmf_iter_row> rows(static_cast<size_t>(config.outer_iters));
@@ -134,7 +136,7 @@ inline std::pair<parmf::FactorModel<float>, parmf::TrainReport> als_train(
     check(pmf_als_train(&c, &v, probe_ptr(probe), static_cast<int64_t>(probe.size()), model.w().data(),
                         model.h().data(), rows.data(), &tot));
     return {std::move(model), detail::report_of("als", config.k, static_cast<double>(config.lambda),
-                                                config.outer_iters, 1, config.seed, a, rows, tot)};
+                                                config.outer_iters, 1, config.workers, config.seed, a, rows, tot)};
 }
 
 // bench.hpp:44-74 (float only)

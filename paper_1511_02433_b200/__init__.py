@@ -111,6 +111,7 @@ _SIGS = {
     "pmf_objective": ([_P, _P, _P, C.c_int32, C.c_double, _P], C.c_int),
     "pmf_ctx_create": ([_P, C.c_int32, _P], C.c_int),
     "pmf_ctx_create_dist": ([_P, C.c_int32, C.c_int32, C.c_int32, _P, _P], C.c_int),
+    "pmf_ctx_create_group": ([_P, C.c_int32, _P, _P], C.c_int),
     "pmf_ctx_destroy": ([_P], C.c_int),
     "pmf_ctx_ccdpp_begin": ([_P, _P], C.c_int),
     "pmf_ctx_ccdpp_iterate": ([_P, C.c_int32, _P], C.c_int),
@@ -709,10 +710,21 @@ def top_n(model: FactorModel, *args):
 class Context:
     """Matrix resident in HBM (pmf_ctx); CCD++ / ALS state, metrics and model I/O."""
 
-    def __init__(self, a: RatingsMatrix, device: int = -1, rank: int = 0, world: int = 1, nccl_id: bytes = None):
+    def __init__(self, a: RatingsMatrix, device: int = -1, rank: int = 0, world: int = 1, nccl_id: bytes = None,
+                 gpus: int = 1, devices=None):
+        """One device (default), one rank of a multi-process NCCL job (rank / world / nccl_id), or a
+        device group of `gpus` ranks driven by this process (pmf_ctx_create_group; `devices` lists
+        each rank's device, default rank mod device_count())."""
         self.a = a
         self.h = C.c_void_p()
-        if nccl_id is None:
+        if gpus != 1 or devices is not None:
+            if gpus < 1:
+                raise ValueError("workers must be >= 1")
+            dv = None if devices is None else np.ascontiguousarray(devices, np.int32)
+            if dv is not None and len(dv) != gpus:
+                raise ValueError("devices must list one device per rank")
+            _check(lib.pmf_ctx_create_group(a.view(), gpus, _ptr(dv), C.byref(self.h)))
+        elif nccl_id is None:
             _check(lib.pmf_ctx_create(a.view(), device, C.byref(self.h)))
         else:
             idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)

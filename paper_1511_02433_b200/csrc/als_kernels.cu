@@ -126,88 +126,6 @@ __device__ bool warp_cholesky_solve(float* G, int k, float& b0, float& b1) {
     return true;
 }
 
-// warp_cholesky_solve for k == K known at compile time (the tensor-core kernels' padded order): every
-// loop is unrolled, so the dot products read G with immediate offsets and carry no loop or bounds
-// bookkeeping.  Same arithmetic and order as warp_cholesky_solve.  Opt-in (PMF_ALS_EXACT=1): the
-// unrolled code outgrows the instruction cache and measured 2 % slower at Netflix k = 40.
-template <int K, int GS>
-__device__ __forceinline__ bool warp_cholesky_solve_exact(float* G, float& b0, float& b1) {
-    const int lane = threadIdx.x & 31;
-    bool ok = true;
-#pragma unroll
-    for (int j = 0; j < K; ++j) {
-        const int i0 = j + 1 + lane, i1 = i0 + 32;
-        const bool h0 = i0 < K, h1 = i1 < K;
-        const float* Gj = G + j * GS;
-        const float* G0 = G + (h0 ? i0 : j) * GS;
-        const float* G1 = G + (h1 ? i1 : j) * GS;
-        float d0 = Gj[j], d1 = 0.f, d2 = 0.f, d3 = 0.f;
-        float s0 = h0 ? G0[j] : 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-        float r0 = h1 ? G1[j] : 0.f, r1 = 0.f;
-#pragma unroll
-        for (int t = 0; t + 4 <= j; t += 4) {
-            const float g0 = Gj[t], g1 = Gj[t + 1], g2 = Gj[t + 2], g3 = Gj[t + 3];
-            d0 = fmaf(-g0, g0, d0);
-            d1 = fmaf(-g1, g1, d1);
-            d2 = fmaf(-g2, g2, d2);
-            d3 = fmaf(-g3, g3, d3);
-            s0 = fmaf(-G0[t], g0, s0);
-            s1 = fmaf(-G0[t + 1], g1, s1);
-            s2 = fmaf(-G0[t + 2], g2, s2);
-            s3 = fmaf(-G0[t + 3], g3, s3);
-            if (K > 32 && h1) {
-                r0 = fmaf(-G1[t], g0, r0);
-                r1 = fmaf(-G1[t + 1], g1, r1);
-                r0 = fmaf(-G1[t + 2], g2, r0);
-                r1 = fmaf(-G1[t + 3], g3, r1);
-            }
-        }
-#pragma unroll
-        for (int t = j & ~3; t < j; ++t) {
-            const float g0 = Gj[t];
-            d0 = fmaf(-g0, g0, d0);
-            s0 = fmaf(-G0[t], g0, s0);
-            if (K > 32 && h1) r0 = fmaf(-G1[t], g0, r0);
-        }
-        const float d = (d0 + d1) + (d2 + d3);
-        if (!(d > 0.f)) {
-            ok = false;
-            break;
-        }
-        const float ljj = sqrtf(d);
-        const float rl = 1.0f / ljj;
-        __syncwarp();
-        if (h0) G[i0 * GS + j] = ((s0 + s1) + (s2 + s3)) * rl;
-        if (K > 32 && h1) G[i1 * GS + j] = (r0 + r1) * rl;
-        if (lane == 0) G[j * GS + j] = ljj;
-        __syncwarp();
-    }
-    if (!ok) return false;
-#pragma unroll
-    for (int i = 0; i < K; ++i) {
-        const float bi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
-        const float yi = bi / G[i * GS + i];
-        if (lane == (i & 31)) {
-            if (i < 32) b0 = yi;
-            else b1 = yi;
-        }
-        if (lane > i && lane < K) b0 = fmaf(-G[lane * GS + i], yi, b0);
-        if (K > 32 && lane + 32 > i && lane + 32 < K) b1 = fmaf(-G[(lane + 32) * GS + i], yi, b1);
-    }
-#pragma unroll
-    for (int i = K - 1; i >= 0; --i) {
-        const float yi = __shfl_sync(0xffffffffu, i < 32 ? b0 : b1, i & 31);
-        const float xi = yi / G[i * GS + i];
-        if (lane == (i & 31)) {
-            if (i < 32) b0 = xi;
-            else b1 = xi;
-        }
-        if (lane < i) b0 = fmaf(-G[i * GS + lane], xi, b0);
-        if (K > 32 && lane + 32 < i) b1 = fmaf(-G[i * GS + lane + 32], xi, b1);
-    }
-    return true;
-}
-
 // warp_cholesky_solve for the tensor-core kernels' gram (row stride GS: 16-byte rows, GS / 4 odd):
 // the lane's row and the pivot row are read 4 columns at a time with 128-bit loads (the pivot row is a
 // broadcast, the lanes' rows are conflict-free), the second row set of a lane (i0 + 32) is only
@@ -528,7 +446,7 @@ __global__ void __launch_bounds__(kTcThreads, PMF_TC_MINB)
 als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_t* __restrict__ idx,
                    const float* __restrict__ val, const float* __restrict__ opp, float* __restrict__ out,
                    int32_t out_off, int k, float lambda, int weighted, float* __restrict__ partial,
-                   int* __restrict__ counter, int* __restrict__ status, int tma, int exact, int gs,
+                   int* __restrict__ counter, int* __restrict__ status, int tma, int gs,
                    const __grid_constant__ CUtensorMap rows_map) {
     using T = TcGeo<NT, MT>;
     constexpr int KS = T::KS, JN = T::JN, NTILES = T::NTILES, KMAX = T::KMAX;
@@ -749,9 +667,7 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
             __syncwarp();
             continue;
         }
-        const bool ok = exact == 2 ? true  // timing experiment only (PMF_ALS_EXACT=2): no factorisation
-                        : (exact && k == KMAX) ? warp_cholesky_solve_exact<KMAX, GS>(G, rhs0, rhs1)
-                                               : warp_cholesky_solve_v4<KMAX, GS>(G, k, rhs0, rhs1);
+        const bool ok = warp_cholesky_solve_v4<KMAX, GS>(G, k, rhs0, rhs1);
         if (!ok) {
             if (lane == 0) atomicExch(status, 4);
             rhs0 = rhs1 = 0.f;
@@ -867,11 +783,6 @@ bool use_tensor_cores() {
     return tc;
 }
 
-int als_exact_chol() {
-    static const int on = std::getenv("PMF_ALS_EXACT") != nullptr ? std::atoi(std::getenv("PMF_ALS_EXACT")) : 0;
-    return on;
-}
-
 using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -923,7 +834,7 @@ void launch_tc(const DevAls& L, const float* opp, int64_t n_opp, float* out, int
     if (tma && mode == 2 && k == TcGeo<NT, MT>::KS && make_rows_map(&map, opp, n_opp, k)) tma = 2;
     als_gram_tc_kernel<NT, MT><<<blocks, kTcThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off,
                                                                 k, lambda, weighted ? 1 : 0, L.partial, d_counter,
-                                                                d_status, tma, als_exact_chol(), gs ? 1 : 0, map);
+                                                                d_status, tma, gs ? 1 : 0, map);
 }
 
 template <int KMAX>

@@ -33,8 +33,8 @@ constexpr int kDefaultPromoteVariant = 0;
 
 // Launch variants (threads per CTA, unroll of the long / medium / short length classes).  More
 // resident warps keep more loads in flight (scripts/micro/stream_bw.cu: 8 warps/SM cap at ~4 TB/s,
-// 16 at ~6.5, 32 at ~6.9); larger unrolls need more registers.  PMF_SWEEP_VARIANT overrides the
-// default for tuning.
+// 16 at ~6.5, 32 at ~6.9); larger unrolls need more registers.  Round 1 also measured 768-thread
+// CTAs, a software-pipelined plain sweep and larger short-class unrolls: all slower, removed.
 template <int V>
 struct Var;
 template <>
@@ -49,36 +49,6 @@ template <>
 struct Var<2> {
     static constexpr int NT = 1024, UA = 2, UB = 2, UC = 2;
 };
-template <>
-struct Var<3> {
-    static constexpr int NT = 768, UA = 4, UB = 4, UC = 2;
-};
-// Software-pipelined plain sweeps (run_class_pipe): the next step's loads are in flight while the
-// current step is reduced, so each lane needs half the unroll for the same bytes in flight.
-template <>
-struct Var<4> {
-    static constexpr int NT = 1024, UA = 2, UB = 2, UC = 1;
-};
-template <>
-struct Var<5> {
-    static constexpr int NT = 1024, UA = 2, UB = 1, UC = 1;
-};
-template <>
-struct Var<6> {
-    static constexpr int NT = 512, UA = 4, UB = 4, UC = 2;
-};
-// Short-segment layouts (Yahoo-Music): more independent loads in flight for the short classes.
-template <>
-struct Var<7> {
-    static constexpr int NT = 1024, UA = 4, UB = 4, UC = 4;
-};
-template <>
-struct Var<8> {
-    static constexpr int NT = 1024, UA = 2, UB = 4, UC = 4;
-};
-template <int V>
-constexpr bool kPipelined = V >= 4 && V <= 6;
-
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
@@ -115,39 +85,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 // Streaming loads of read-only data (indices always; the residual in plain sweeps): ld.global.cs.
-// -DPMF_STREAM_NOALLOC selects ld.global.nc.L1::no_allocate (measured slower: wide-panel v-sweep
-// 188 -> 208 us, Yahoo sweeps +20 %).
-__device__ __forceinline__ float4 ld_stream(const float4* p) {
-#ifndef PMF_STREAM_NOALLOC
-    return __ldcs(p);
-#else
-    float4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
-                 : "l"(p));
-    return v;
-#endif
-}
-__device__ __forceinline__ uint2 ld_stream(const uint2* p) {
-#ifndef PMF_STREAM_NOALLOC
-    return __ldcs(p);
-#else
-    uint2 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(p));
-    return v;
-#endif
-}
-__device__ __forceinline__ int4 ld_stream(const int4* p) {
-#ifndef PMF_STREAM_NOALLOC
-    return __ldcs(p);
-#else
-    int4 v;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.s32 {%0,%1,%2,%3}, [%4];"
-                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
-                 : "l"(p));
-    return v;
-#endif
-}
+// (ld.global.nc.L1::no_allocate measured slower in round 1: wide-panel v-sweep 188 -> 208 us.)
+__device__ __forceinline__ float4 ld_stream(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ uint2 ld_stream(const uint2* p) { return __ldcs(p); }
+__device__ __forceinline__ int4 ld_stream(const int4* p) { return __ldcs(p); }
 
 template <bool IDX16>
 struct IdxVec;
@@ -377,136 +318,6 @@ __device__ __noinline__ void run_rmw_sub(int* counter, int32_t ub, int32_t ue, c
     }
 }
 
-// Plain-sweep variant of run_class with the loads software-pipelined across steps and unit
-// batches: a warp walks the flattened sequence of (batch, step) pairs and issues the loads of the
-// next pair before gathering and accumulating the current one, so its loads are in flight
-// continuously instead of only between batches.  Same per-unit arithmetic and reduction order as
-// run_class (bitwise identical results).
-template <bool IDX16, int G, int kUnroll>
-struct PipeBuf {
-    float4 r[kUnroll];
-    typename IdxVec<IDX16>::raw_t ix[kUnroll];
-    int rem;
-};
-
-template <bool IDX16, int G, int kUnroll>
-__device__ __forceinline__ void pipe_load(PipeBuf<IDX16, G, kUnroll>& b, const Unit& U, int s, int gl,
-                                          const void* __restrict__ idx, const float* __restrict__ R) {
-    const int64_t base = static_cast<int64_t>(U.e0) + 4 * (gl + G * kUnroll * s);
-    b.rem = static_cast<int>(static_cast<int64_t>(U.e0) + U.len - base);
-    const float4* rp = reinterpret_cast<const float4*>(R + base);
-    const typename IdxVec<IDX16>::raw_t* ip = reinterpret_cast<const typename IdxVec<IDX16>::raw_t*>(
-        static_cast<const char*>(idx) + base * (IDX16 ? 2 : 4));
-    // every register of the buffer is redefined (zero past the end), so no value of the previous
-    // stage stays live across the loop
-#pragma unroll
-    for (int q = 0; q < kUnroll; ++q) {
-        const bool in = 4 * G * q < b.rem;
-        b.r[q] = in ? ld_stream(rp + G * q) : make_float4(0.f, 0.f, 0.f, 0.f);
-        b.ix[q] = in ? ld_stream(ip + G * q) : typename IdxVec<IDX16>::raw_t{};
-    }
-}
-
-template <bool IDX16, int G, int kUnroll>
-__device__ __forceinline__ void pipe_accumulate(const PipeBuf<IDX16, G, kUnroll>& b, const float* g0, float& num,
-                                                float& den) {
-    using IV = IdxVec<IDX16>;
-#pragma unroll
-    for (int q = 0; q < kUnroll; ++q)
-        if (4 * G * q < b.rem) {
-            const float rv[4] = {b.r[q].x, b.r[q].y, b.r[q].z, b.r[q].w};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const float gv = g0[IV::get(b.ix[q], c)];
-                num = fmaf(rv[c], gv, num);
-                den = fmaf(gv, gv, den);
-            }
-        }
-}
-
-// State of one warp's walk over its (batch, step) sequence.
-struct PipeState {
-    Unit U, Un;    // current batch's unit (per group) and the next batch's (prefetched)
-    int nbn;       // first unit index of the next batch
-    int steps, s;  // group-steps of the current batch (warp maximum) and the current step
-    float num, den;
-};
-
-template <bool IDX16, int G, int kUnroll>
-__device__ __forceinline__ void pipe_grab(int* counter, int32_t ue, const Unit* __restrict__ units, int& nb,
-                                          Unit& u) {
-    const int lane = threadIdx.x & 31;
-    if (lane == 0) nb = atomicAdd(counter, 32 / G);
-    nb = __shfl_sync(0xffffffffu, nb, 0);
-    u = (nb + lane / G < ue) ? units[nb + lane / G] : Unit{0u, 0, 0, -2};
-}
-
-template <int G, int kUnroll>
-__device__ __forceinline__ int pipe_steps(const Unit& u) {
-    constexpr int SE = 4 * G * kUnroll;
-    const int my = (u.len + SE - 1) / SE;
-    return max(1, static_cast<int>(__reduce_max_sync(0xffffffffu, static_cast<unsigned>(my))));
-}
-
-// One pipeline stage: prefetch the next (batch, step) into `nx`, consume `cur`.  Returns false when
-// the warp has no further batch.
-template <bool IDX16, int G, int kUnroll>
-__device__ __forceinline__ bool pipe_stage(PipeState& st, PipeBuf<IDX16, G, kUnroll>& cur,
-                                           PipeBuf<IDX16, G, kUnroll>& nx, int* counter, int32_t ue,
-                                           const Unit* __restrict__ units, const void* __restrict__ idx,
-                                           const float* __restrict__ R, float2* __restrict__ partial,
-                                           const SweepOperands& op, const float* g0) {
-    const int gl = (threadIdx.x & 31) % G;
-    const bool adv = st.s + 1 >= st.steps;
-    if (adv) pipe_load(nx, st.Un, 0, gl, idx, R);  // Un.len == 0 past the end: no loads
-    else pipe_load(nx, st.U, st.s + 1, gl, idx, R);
-    pipe_accumulate(cur, g0, st.num, st.den);
-    if (!adv) {
-        ++st.s;
-        return true;
-    }
-    float num = st.num, den = st.den;
-#pragma unroll
-    for (int off = G / 2; off > 0; off >>= 1) {
-        num += __shfl_xor_sync(0xffffffffu, num, off);
-        den += __shfl_xor_sync(0xffffffffu, den, off);
-    }
-    if (gl == 0 && st.U.len > 0) {
-        if (st.U.slot < 0) {
-            const float dt = __fadd_rn(op.lambda, den);
-            op.out[op.out_off + st.U.o] = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
-        } else {
-            partial[st.U.slot] = make_float2(num, den);
-        }
-    }
-    st.num = st.den = 0.f;
-    if (st.nbn >= ue) return false;
-    st.U = st.Un;
-    st.steps = pipe_steps<G, kUnroll>(st.U);
-    st.s = 0;
-    pipe_grab<IDX16, G, kUnroll>(counter, ue, units, st.nbn, st.Un);
-    return true;
-}
-
-template <bool IDX16, int G, int kUnroll>
-__device__ __forceinline__ void run_class_pipe(int* counter, int32_t ub, int32_t ue, const Unit* __restrict__ units,
-                                            const void* __restrict__ idx, const float* __restrict__ R,
-                                            float2* __restrict__ partial, const SweepOperands& op,
-                                            const float* g0) {
-    if (ub >= ue) return;
-    PipeState st;
-    int nb;
-    pipe_grab<IDX16, G, kUnroll>(counter, ue, units, nb, st.U);
-    if (nb >= ue) return;
-    pipe_grab<IDX16, G, kUnroll>(counter, ue, units, st.nbn, st.Un);
-    st.steps = pipe_steps<G, kUnroll>(st.U);
-    st.s = 0;
-    st.num = st.den = 0.f;
-    PipeBuf<IDX16, G, kUnroll> cur, nx;
-    pipe_load(cur, st.U, 0, (threadIdx.x & 31) % G, idx, R);
-    // the loop-carried buffer is renamed, not copied, once the loop is in SSA form
-    while (pipe_stage(st, cur, nx, counter, ue, units, idx, R, partial, op, g0)) cur = nx;
-}
 
 template <int MODE, bool CSR, bool IDX16, bool SMEM, int V>
 __global__ void __launch_bounds__(Var<V>::NT, 1)
@@ -626,15 +437,9 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
                     continue;
                 }
             }
-            if constexpr (MODE == kPlain && kPipelined<V>) {
-                run_class_pipe<IDX16, 8, Var<V>::UA>(c0, pz.ub, pz.um, units, idx, R, partial, op, g0);
-                run_class_pipe<IDX16, 4, Var<V>::UB>(c1, pz.um, pz.us, units, idx, R, partial, op, g0);
-                run_class_pipe<IDX16, 2, Var<V>::UC>(c2, pz.us, pz.ue, units, idx, R, partial, op, g0);
-            } else {
-                run_class<MODE, CSR, IDX16, 8, Var<V>::UA>(c0, pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
-                run_class<MODE, CSR, IDX16, 4, Var<V>::UB>(c1, pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
-                run_class<MODE, CSR, IDX16, 2, Var<V>::UC>(c2, pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
-            }
+            run_class<MODE, CSR, IDX16, 8, Var<V>::UA>(c0, pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
+            run_class<MODE, CSR, IDX16, 4, Var<V>::UB>(c1, pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
+            run_class<MODE, CSR, IDX16, 2, Var<V>::UC>(c2, pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
         }
     }
     if (steal) {
@@ -762,29 +567,12 @@ void launch_one(const DevSweep& L, const SweepOperands& op, size_t smem, cudaStr
         L.n_pieces);
 }
 
+// plain sweeps: 1024 threads (u-sweep unroll 4/2/2, v-sweep 2/2/2); promote: 512 threads, 8/4/4;
+// split-promote residual pass: 1024 threads, 2/2/2
 int variant_for(int mode, bool csr) {
-    // PMF_SWEEP_VARIANT (both sides) / PMF_SWEEP_VARIANT_CSR / _CSC override the plain-sweep default
-    static const int plain_csr = [] {
-        const char* e = std::getenv("PMF_SWEEP_VARIANT_CSR");
-        if (!e) e = std::getenv("PMF_SWEEP_VARIANT");
-        return e ? std::atoi(e) : kDefaultPlainVariantCsr;
-    }();
-    static const int plain_csc = [] {
-        const char* e = std::getenv("PMF_SWEEP_VARIANT_CSC");
-        if (!e) e = std::getenv("PMF_SWEEP_VARIANT");
-        return e ? std::atoi(e) : kDefaultPlainVariantCsc;
-    }();
-    const int plain = csr ? plain_csr : plain_csc;
-    static const int promote = [] {
-        const char* e = std::getenv("PMF_PROMOTE_VARIANT");
-        return e ? std::atoi(e) : kDefaultPromoteVariant;
-    }();
-    static const int rmw = [] {
-        const char* e = std::getenv("PMF_RMW_VARIANT");
-        return e ? std::atoi(e) : 2;
-    }();
-    if (mode == kRmw) return rmw;
-    return mode == kPlain ? plain : promote;
+    if (mode == kRmw) return 2;
+    if (mode == kPlain) return csr ? kDefaultPlainVariantCsr : kDefaultPlainVariantCsc;
+    return kDefaultPromoteVariant;
 }
 
 template <int MODE, bool CSR>
@@ -793,18 +581,7 @@ void dispatch_idx(const DevSweep& L, const SweepOperands& op, size_t smem, cudaS
         switch (variant_for(MODE, CSR)) {
             case 1: launch_one<MODE, CSR, true, true, 1>(L, op, smem, s); return;
             case 2: launch_one<MODE, CSR, true, true, 2>(L, op, smem, s); return;
-            case 3: launch_one<MODE, CSR, true, true, 3>(L, op, smem, s); return;
             default: break;
-        }
-        if constexpr (MODE == kPlain) {
-            switch (variant_for(MODE, CSR)) {
-                case 4: launch_one<MODE, CSR, true, true, 4>(L, op, smem, s); return;
-                case 5: launch_one<MODE, CSR, true, true, 5>(L, op, smem, s); return;
-                case 6: launch_one<MODE, CSR, true, true, 6>(L, op, smem, s); return;
-                case 7: launch_one<MODE, CSR, true, true, 7>(L, op, smem, s); return;
-                case 8: launch_one<MODE, CSR, true, true, 8>(L, op, smem, s); return;
-                default: break;
-            }
         }
         launch_one<MODE, CSR, true, true, 0>(L, op, smem, s);
         return;
@@ -825,14 +602,6 @@ void set_attr_all(size_t max_smem) {
     set_attr<MODE, CSR, true, true, 0>(max_smem);
     set_attr<MODE, CSR, true, true, 1>(max_smem);
     set_attr<MODE, CSR, true, true, 2>(max_smem);
-    set_attr<MODE, CSR, true, true, 3>(max_smem);
-    if constexpr (MODE == kPlain) {
-        set_attr<MODE, CSR, true, true, 4>(max_smem);
-        set_attr<MODE, CSR, true, true, 5>(max_smem);
-        set_attr<MODE, CSR, true, true, 6>(max_smem);
-        set_attr<MODE, CSR, true, true, 7>(max_smem);
-        set_attr<MODE, CSR, true, true, 8>(max_smem);
-    }
     set_attr<MODE, CSR, true, false, 0>(max_smem);
     set_attr<MODE, CSR, false, true, 0>(max_smem);
     set_attr<MODE, CSR, false, false, 0>(max_smem);

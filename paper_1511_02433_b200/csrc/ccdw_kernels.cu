@@ -172,7 +172,30 @@ ccd_cols_kernel(const int64_t* __restrict__ col_start, const int32_t* __restrict
     }
 }
 
+// R = A - W H^T from scratch (a warp per row; t ascending, each product rounded before the subtract):
+// the residual of a model installed with set_model (residual_from + the writebacks' arithmetic).
+__global__ void ccd_residual_kernel(const int64_t* __restrict__ row_start, const int32_t* __restrict__ col_of,
+                                    const float* __restrict__ A, const float* __restrict__ W,
+                                    const float* __restrict__ H, int32_t m, int k, float* __restrict__ R) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < m;
+         i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
+        const float* w = W + i * k;
+        for (int64_t p = row_start[i] + lane; p < row_start[i + 1]; p += 32) {
+            const float* h = H + static_cast<int64_t>(col_of[p]) * k;
+            float r = A[p];
+            for (int t = 0; t < k; ++t) r = __fsub_rn(r, __fmul_rn(w[t], h[t]));
+            R[p] = r;
+        }
+    }
+}
+
 }  // namespace
+
+void launch_ccd_residual(const CcdWs& ws, const float* A_row, const float* W, const float* H, int k, cudaStream_t s) {
+    if (ws.m > 0) ccd_residual_kernel<<<148 * 8, 256, 0, s>>>(ws.row_start, ws.col_of, A_row, W, H, ws.m, k, ws.R_row);
+    if (ws.nnz > 0) ccd_gather_kernel<<<148 * 16, 256, 0, s>>>(ws.R_col, ws.R_row, ws.csc2csr, ws.nnz);
+}
 
 void launch_ccd_xlinks(const int64_t* row_start, const int32_t* col_of, const int64_t* col_start,
                        const int32_t* row_of, int32_t m, int32_t* csr2csc, int32_t* csc2csr, cudaStream_t s) {

@@ -119,6 +119,8 @@ void launch_ccd_xlinks(const int64_t* row_start, const int32_t* col_of, const in
                        const int32_t* row_of, int32_t m, int32_t* csr2csc, int32_t* csc2csr, cudaStream_t s);
 // One epoch (W sweep, mirror, H sweep, mirror) on row-major W (m x k) / H (n x k).  Returns launches.
 int launch_ccd_epoch(const CcdWs& ws, float* W, float* H, int k, float lambda, cudaStream_t s);
+// R_row = A - W H^T (t ascending, products rounded before the subtracts), mirrored into R_col.
+void launch_ccd_residual(const CcdWs& ws, const float* A_row, const float* W, const float* H, int k, cudaStream_t s);
 
 // ---- top_n (model.hpp:172-209), topn_kernels.cu ------------------------------------------------
 // For each of n_users users (W rows users[u]): the `count` best unrated items of W H^T (row-major
@@ -126,6 +128,13 @@ int launch_ccd_epoch(const CcdWs& ws, float* W, float* H, int k, float lambda, c
 // n_users x count (items -1 past out_count[u]).
 size_t topn_smem_bytes(int k, int count);
 void topn_set_attributes(size_t max_smem);
+// Any count / k: batches of `batch` users, full scoring + stable segmented radix sort (scratch from
+// topn_wide_scratch_bytes).
+int topn_wide_batch(int32_t n);
+size_t topn_wide_scratch_bytes(int32_t n, int batch);
+cudaError_t launch_topn_wide(const float* W, const float* H, int32_t n, int k, const int32_t* users, int32_t n_users,
+                             const int64_t* ex_start, const int32_t* ex_items, int count, int32_t* out_items,
+                             float* out_scores, int32_t* out_count, void* scratch, int batch, cudaStream_t s);
 void launch_topn(const float* W, const float* H, int32_t n, int k, const int32_t* users, int32_t n_users,
                  const int64_t* ex_start, const int32_t* ex_items, int count, int32_t* out_items, float* out_scores,
                  int32_t* out_count, cudaStream_t s);

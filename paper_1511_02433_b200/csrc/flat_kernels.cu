@@ -29,53 +29,9 @@ namespace {
 
 enum FlatMode { kFPlain = 0, kFDemote = 1, kFBuild = 2, kFBuildSweep = 3 };
 
-// Launch variants: threads per CTA, 32-vector blocks loaded per warp iteration (loads in flight).
-// PMF_FLAT_VARIANT selects one for tuning.
-template <int V>
-struct FVar;
-template <>
-struct FVar<0> {
-    static constexpr int NT = 1024, NB = 2;
-};
-template <>
-struct FVar<1> {
-    static constexpr int NT = 1024, NB = 3;
-};
-template <>
-struct FVar<2> {
-    static constexpr int NT = 512, NB = 4;
-};
-template <>
-struct FVar<3> {
-    static constexpr int NT = 512, NB = 6;
-};
-template <>
-struct FVar<4> {
-    static constexpr int NT = 768, NB = 3;
-};
-// software-pipelined: the next block's loads (across chunk boundaries) are in flight while the
-// current block is processed
-template <>
-struct FVar<5> {
-    static constexpr int NT = 512, NB = 1, PIPE = 1;
-};
-template <>
-struct FVar<6> {
-    static constexpr int NT = 768, NB = 1, PIPE = 1;
-};
-template <>
-struct FVar<7> {
-    static constexpr int NT = 1024, NB = 1, PIPE = 1;
-};
-template <int V, class = void>
-struct IsPipe {
-    static constexpr bool value = false;
-};
-template <int V>
-struct IsPipe<V, decltype(void(FVar<V>::PIPE))> {
-    static constexpr bool value = FVar<V>::PIPE != 0;
-};
-constexpr int kDefaultFlatVariant = 0;
+// 1024 threads per CTA, one CTA per SM.  Round 1 measured 512 / 768-thread CTAs, more 32-vector
+// blocks in flight per warp and a software-pipelined (chunk, block) sequence: all slower, removed.
+constexpr int kFlatThreads = 1024;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -358,8 +314,8 @@ struct FlatClaim {
     }
 };
 
-template <int FM, bool CSR, int V>
-__global__ void __launch_bounds__(FVar<V>::NT, 1)
+template <int FM, bool CSR>
+__global__ void __launch_bounds__(kFlatThreads, 1)
 flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, const int32_t* __restrict__ piece_start,
             const int32_t* __restrict__ panel_base, const FlatChunk* __restrict__ chunks,
             const uint32_t* __restrict__ tb, const uint16_t* __restrict__ idx, float* __restrict__ R,
@@ -438,77 +394,23 @@ flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, co
         // descriptors / tail words, chunk i+2's descriptor and the claim of chunk i+3 are in flight.
         const int cend = pz.pad[1];
         const FlatChunk none{0, 0, 0, 0};
-        if constexpr (IsPipe<V>::value) {
-            int a = 0;
-            if (lane == 0) a = atomicAdd(counter, 1);
-            int c1 = __shfl_sync(0xffffffffu, a, 0);
-            if (lane == 0) a = atomicAdd(counter, 1);
-            int c2 = __shfl_sync(0xffffffffu, a, 0);
-            FlatChunk ch1 = c1 < cend ? chunks[c1] : none;
-            FlatChunk ch2 = c2 < cend ? chunks[c2] : none;
-            if (lane == 0) a = atomicAdd(counter, 1);
-            ChunkInfo ci1 = chunk_info<FM>(ch1, units, tb, op);
-            // (chunk, block) pairs in sequence; the loads of the next pair -- the current chunk's
-            // next block or the next chunk's first -- are issued before the current one is processed
-            ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
-            int c3 = __shfl_sync(0xffffffffu, a, 0);
-            FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
-            if (lane == 0) a = atomicAdd(counter, 1);
-            float r[16], rn[16];
-            uint32_t ix[8], ixn[8];
-            int vb = ch1.v0 & ~3;
-            if (c1 < cend) load_block(r, ix, ch1, vb, idx, R);
-            float cn = 0.f, cd = 0.f;
-            int ucur = 0;
-            while (c1 < cend) {
-                const int nvb = vb + 128;
-                const bool same = nvb < ch1.v1;
-                if (same) load_block(rn, ixn, ch1, nvb, idx, R);
-                else if (c2 < cend) load_block(rn, ixn, ch2, ch2.v0 & ~3, idx, R);
-                flat_block<FM, CSR>(r, ix, ch1, ci1, vb, cn, cd, ucur, R, partial, op, smem, panel_size);
-                if (same) {
-                    vb = nvb;
-                } else {
-                    const ChunkInfo ci3 = chunk_info<FM>(ch3, units, tb, op);  // ch3 loaded a chunk ago
-                    const int c4 = __shfl_sync(0xffffffffu, a, 0);
-                    const FlatChunk ch4 = c4 < cend ? chunks[c4] : none;
-                    if (lane == 0) a = atomicAdd(counter, 1);
-                    c1 = c2;
-                    ch1 = ch2;
-                    ci1 = ci2;
-                    c2 = c3;
-                    ch2 = ch3;
-                    ci2 = ci3;
-                    c3 = c4;
-                    ch3 = ch4;
-                    vb = ch1.v0 & ~3;
-                    cn = cd = 0.f;
-                    ucur = 0;
-                }
-#pragma unroll
-                for (int q = 0; q < 16; ++q) r[q] = rn[q];
-#pragma unroll
-                for (int q = 0; q < 8; ++q) ix[q] = ixn[q];
-            }
-        } else {
-            // chunks are claimed in pairs (one atomic per two chunks), a pair ahead of use
-            FlatClaim cl{counter, 0, -1};
-            cl.issue();
-            int c1 = cl.next(), c2 = cl.next();
-            FlatChunk ch1 = c1 < cend ? chunks[c1] : none;
-            FlatChunk ch2 = c2 < cend ? chunks[c2] : none;
-            ChunkInfo ci1 = chunk_info<FM>(ch1, units, tb, op);
-            while (c1 < cend) {
-                const ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
-                const int c3 = cl.next();
-                const FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
-                flat_chunk<FM, CSR>(ch1, ci1, idx, R, partial, op, smem, panel_size);
-                c1 = c2;
-                ch1 = ch2;
-                ci1 = ci2;
-                c2 = c3;
-                ch2 = ch3;
-            }
+        // chunks are claimed in pairs (one atomic per two chunks), a pair ahead of use
+        FlatClaim cl{counter, 0, -1};
+        cl.issue();
+        int c1 = cl.next(), c2 = cl.next();
+        FlatChunk ch1 = c1 < cend ? chunks[c1] : none;
+        FlatChunk ch2 = c2 < cend ? chunks[c2] : none;
+        ChunkInfo ci1 = chunk_info<FM>(ch1, units, tb, op);
+        while (c1 < cend) {
+            const ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
+            const int c3 = cl.next();
+            const FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
+            flat_chunk<FM, CSR>(ch1, ci1, idx, R, partial, op, smem, panel_size);
+            c1 = c2;
+            ch1 = ch2;
+            ci1 = ci2;
+            c2 = c3;
+            ch2 = ch3;
         }
     }
     if (steal) {
@@ -543,55 +445,21 @@ int flat_restage_min() {
     return v;
 }
 
-template <int FM, bool CSR, int V>
-void launch_flat_v(const DevSweep& L, const SweepOperands& op, const float* gsrc, bool steal, cudaStream_t s) {
+template <int FM, bool CSR>
+void launch_flat_mode(const DevSweep& L, const SweepOperands& op, const float* gsrc, bool steal,
+                      cudaStream_t s) {
     const size_t smem = static_cast<size_t>(((L.panel_size + 1) + 3) & ~3) * sizeof(float);
-    flat_kernel<FM, CSR, V><<<L.ctas, FVar<V>::NT, smem, s>>>(
+    flat_kernel<FM, CSR><<<L.ctas, kFlatThreads, smem, s>>>(
         L.units, L.pieces, L.piece_start, L.panel_base, L.chunks, L.tailbits, static_cast<const uint16_t*>(L.idx),
         L.R, L.partial, op, gsrc, L.panel_size, steal ? L.gcnt : nullptr, L.n_pieces, flat_restage_min());
 }
 
-int flat_variant() {
-    static const int v = [] {
-        const char* e = std::getenv("PMF_FLAT_VARIANT");
-        return e ? std::atoi(e) : kDefaultFlatVariant;
-    }();
-    return v;
-}
-
-template <int FM, bool CSR>
-void launch_flat_mode(const DevSweep& L, const SweepOperands& op, const float* gsrc, bool steal,
-                      cudaStream_t s) {
-    switch (flat_variant()) {
-        case 1: launch_flat_v<FM, CSR, 1>(L, op, gsrc, steal, s); return;
-        case 2: launch_flat_v<FM, CSR, 2>(L, op, gsrc, steal, s); return;
-        case 3: launch_flat_v<FM, CSR, 3>(L, op, gsrc, steal, s); return;
-        case 4: launch_flat_v<FM, CSR, 4>(L, op, gsrc, steal, s); return;
-        case 5: launch_flat_v<FM, CSR, 5>(L, op, gsrc, steal, s); return;
-        case 6: launch_flat_v<FM, CSR, 6>(L, op, gsrc, steal, s); return;
-        case 7: launch_flat_v<FM, CSR, 7>(L, op, gsrc, steal, s); return;
-        default: launch_flat_v<FM, CSR, 0>(L, op, gsrc, steal, s); return;
-    }
-}
-
-template <int FM, int V>
-void set_flat_attr_v(size_t max_smem) {
-    cudaFuncSetAttribute(flat_kernel<FM, true, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(max_smem));
-    cudaFuncSetAttribute(flat_kernel<FM, false, V>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(max_smem));
-}
-
 template <int FM>
 void set_flat_attr(size_t max_smem) {
-    set_flat_attr_v<FM, 0>(max_smem);
-    set_flat_attr_v<FM, 1>(max_smem);
-    set_flat_attr_v<FM, 2>(max_smem);
-    set_flat_attr_v<FM, 3>(max_smem);
-    set_flat_attr_v<FM, 4>(max_smem);
-    set_flat_attr_v<FM, 5>(max_smem);
-    set_flat_attr_v<FM, 6>(max_smem);
-    set_flat_attr_v<FM, 7>(max_smem);
+    cudaFuncSetAttribute(flat_kernel<FM, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(max_smem));
+    cudaFuncSetAttribute(flat_kernel<FM, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(max_smem));
 }
 
 bool flat_steal() {

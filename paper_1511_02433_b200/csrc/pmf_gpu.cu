@@ -433,11 +433,20 @@ struct Ctx {
     DevMem probe_mem;
     int64_t h2d = 0, d2h = 0;
     double setup_seconds = 0;
+    // Single-process device group (pmf_ctx_create_group, num_gpus > 1 in the whole-call API): rank 0
+    // owns ranks 1..G-1 and drives all of them; `ranks` lists every rank in order (empty otherwise).
+    // The all-gathers are peer copies between the ranks' replicated vectors (see exchange()).
+    std::vector<std::unique_ptr<Ctx>> peers;
+    std::vector<Ctx*> ranks;
+    cudaEvent_t ev_done = nullptr, ev_sent = nullptr;
 
     ~Ctx() {
+        cudaSetDevice(device);
         if (graph_exec) cudaGraphExecDestroy(graph_exec);
         if (graph) cudaGraphDestroy(graph);
         if (comm) ncclCommDestroy(comm);
+        if (ev_done) cudaEventDestroy(ev_done);
+        if (ev_sent) cudaEventDestroy(ev_sent);
         if (stream) cudaStreamDestroy(stream);
     }
     int32_t prow(int32_t i) const { return rmap.empty() ? i : rmap[i]; }
@@ -561,6 +570,8 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     c->device = device;
     CUDA_TRY(cudaSetDevice(device));
     CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_sent, cudaEventDisableTiming));
     CUDA_TRY(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
     c->m = a->m;
     c->n = a->n;
@@ -697,6 +708,59 @@ void allgather(Ctx& c, float* buf, int64_t block) {
         NCCL_TRY(ncclAllGather(buf + static_cast<int64_t>(c.rank) * block, buf, block, ncclFloat, c.comm, c.stream));
 }
 
+using Ranks = std::vector<Ctx*>;
+Ranks ranks_of(Ctx& c) { return c.ranks.empty() ? Ranks{&c} : c.ranks; }
+
+// All-gather of a replicated vector (block r = `block` floats at r * block, just written by rank r).
+// One rank: NCCL in place (a no-op without a communicator).  A device group: every rank pushes its
+// block into every peer's copy, between two event rounds -- the pushes wait until each peer's last
+// kernel (the last reader of the old contents) is done (ev_done), and each rank's next kernel waits
+// for every push into its copy (ev_sent).  Host-ordered records and waits, so this also captures
+// into a CUDA graph as plain dependencies.
+template <class Buf>
+void exchange(const Ranks& cs, Buf buf, int64_t block) {
+    if (cs.size() == 1) {
+        allgather(*cs[0], buf(*cs[0]), block);
+        return;
+    }
+    for (Ctx* c : cs) CUDA_TRY(cudaEventRecord(c->ev_done, c->stream));
+    for (Ctx* r : cs) {
+        for (Ctx* q : cs)
+            if (q != r) CUDA_TRY(cudaStreamWaitEvent(r->stream, q->ev_done, 0));
+        const int64_t off = static_cast<int64_t>(r->rank) * block;
+        for (Ctx* q : cs)
+            if (q != r)
+                CUDA_TRY(cudaMemcpyAsync(buf(*q) + off, buf(*r) + off, sizeof(float) * block, cudaMemcpyDefault,
+                                         r->stream));
+        CUDA_TRY(cudaEventRecord(r->ev_sent, r->stream));
+    }
+    for (Ctx* q : cs)
+        for (Ctx* r : cs)
+            if (r != q) CUDA_TRY(cudaStreamWaitEvent(q->stream, r->ev_sent, 0));
+}
+
+// rank 0's stream forks to / joins from the other ranks' streams (a group's work is one graph,
+// launched and timed on rank 0's stream)
+void fork_ranks(const Ranks& cs) {
+    if (cs.size() == 1) return;
+    CUDA_TRY(cudaEventRecord(cs[0]->ev_done, cs[0]->stream));
+    for (size_t r = 1; r < cs.size(); ++r) CUDA_TRY(cudaStreamWaitEvent(cs[r]->stream, cs[0]->ev_done, 0));
+}
+void join_ranks(const Ranks& cs) {
+    if (cs.size() == 1) return;
+    for (size_t r = 1; r < cs.size(); ++r) {
+        CUDA_TRY(cudaEventRecord(cs[r]->ev_done, cs[r]->stream));
+        CUDA_TRY(cudaStreamWaitEvent(cs[0]->stream, cs[r]->ev_done, 0));
+    }
+}
+// a group's schedule is captured as one graph when all its ranks share a device (streams of
+// several devices run it uncaptured, issued from the host)
+bool capturable(const Ranks& cs) {
+    for (Ctx* c : cs)
+        if (c->device != cs[0]->device) return false;
+    return true;
+}
+
 struct SweepTimer {
     Ctx& c;
     cudaEvent_t a = nullptr, b = nullptr;
@@ -730,104 +794,101 @@ struct SweepTimer {
     }
 };
 
-// First sweep of a step: fused promote kernel, or a separate residual pass + plain sweep
-// (PMF_SPLIT_PROMOTE = bitmask: 1 = CSR side, 2 = CSC side).
-bool split_promote(bool csr) {
-    static const int mask = [] {
-        const char* e = std::getenv("PMF_SPLIT_PROMOTE");
-        return e ? std::atoi(e) : 0;
-    }();
-    return (mask & (csr ? 1 : 2)) != 0;
-}
-
-// Enqueues one CCD++ outer iteration (ccd.hpp:373-393) on c.stream; returns kernels launched.
-int64_t enqueue_ccd_iteration(Ctx& c) {
+// Enqueues one CCD++ outer iteration (ccd.hpp:373-393) on the ranks' streams; returns kernels launched.
+int64_t enqueue_ccd_iteration(const Ranks& cs) {
     int64_t launched = 0;
-    const int k = c.k;
-    SweepTimer tm(c);
+    Ctx& c0 = *cs[0];
+    const int k = c0.k;
+    SweepTimer tm(c0);  // profiling: rank 0's sweeps
+    fork_ranks(cs);
     for (int t = 0; t < k; ++t) {
         const int tp = (t + k - 1) % k;
-        float* Wt = c.W + static_cast<int64_t>(t) * c.ldm;
-        float* Wp = c.W + static_cast<int64_t>(tp) * c.ldm;
-        float* Ht = c.H + static_cast<int64_t>(t) * c.ldn;
-        float* Hp = c.H + static_cast<int64_t>(tp) * c.ldn;
-        for (int s = 0; s < c.inner; ++s) {
-            SweepOperands ou;
-            ou.lambda = c.lambda;
-            ou.out = c.ubuf;
-            ou.out_off = c.rank * c.Bm;
-            if (s == 0) {
-                ou.ga = Hp;  // v'
-                ou.gb = Ht;  // h (also the v of the first u update)
-                ou.gn = Ht;
-                ou.oa = Wp;  // u'
-                ou.ob = Wt;  // w
-            } else {
-                ou.gn = c.vbuf;
-            }
-            tm.start();
-            if (s == 0 && split_promote(true)) {
-                launched += launch_sweep(c.csr, kRmw, true, ou, c.stream);
-                SweepOperands up = ou;
-                up.gn = Ht;
-                launched += launch_sweep(c.csr, kPlain, true, up, c.stream);
-            } else {
+        for (int s = 0; s < c0.inner; ++s) {
+            for (Ctx* cp : cs) {
+                Ctx& c = *cp;
+                SweepOperands ou;
+                ou.lambda = c.lambda;
+                ou.out = c.ubuf;
+                ou.out_off = c.rank * c.Bm;
+                if (s == 0) {
+                    ou.ga = c.H + static_cast<int64_t>(tp) * c.ldn;  // v'
+                    ou.gb = c.H + static_cast<int64_t>(t) * c.ldn;   // h (also the v of the first u update)
+                    ou.gn = ou.gb;
+                    ou.oa = c.W + static_cast<int64_t>(tp) * c.ldm;  // u'
+                    ou.ob = c.W + static_cast<int64_t>(t) * c.ldm;   // w
+                } else {
+                    ou.gn = c.vbuf;
+                }
+                if (cp == &c0) tm.start();
                 launched += launch_sweep(c.csr, s == 0 ? kPromote : kPlain, true, ou, c.stream);
+                if (cp == &c0) tm.stop(true);
             }
-            tm.stop(true);
-            allgather(c, c.ubuf, c.Bm);
-            SweepOperands ov;
-            ov.lambda = c.lambda;
-            ov.out = c.vbuf;
-            ov.out_off = c.rank * c.Bn;
-            ov.gn = c.ubuf;
-            if (s == 0) {
-                ov.ga = Wp;  // u'
-                ov.gb = Wt;  // w
-                ov.oa = Hp;  // v'
-                ov.ob = Ht;  // h
-            }
-            tm.start();
-            if (s == 0 && split_promote(false)) {
-                // residual update as its own streaming pass, then a plain sweep
-                launched += launch_sweep(c.csc, kRmw, false, ov, c.stream);
-                launched += launch_sweep(c.csc, kPlain, false, ov, c.stream);
-            } else {
+            exchange(cs, [](Ctx& c) { return c.ubuf; }, c0.Bm);
+            for (Ctx* cp : cs) {
+                Ctx& c = *cp;
+                SweepOperands ov;
+                ov.lambda = c.lambda;
+                ov.out = c.vbuf;
+                ov.out_off = c.rank * c.Bn;
+                ov.gn = c.ubuf;
+                if (s == 0) {
+                    ov.ga = c.W + static_cast<int64_t>(tp) * c.ldm;  // u'
+                    ov.gb = c.W + static_cast<int64_t>(t) * c.ldm;   // w
+                    ov.oa = c.H + static_cast<int64_t>(tp) * c.ldn;  // v'
+                    ov.ob = c.H + static_cast<int64_t>(t) * c.ldn;   // h
+                }
+                if (cp == &c0) tm.start();
                 launched += launch_sweep(c.csc, s == 0 ? kPromote : kPlain, false, ov, c.stream);
+                if (cp == &c0) tm.stop(false);
             }
-            tm.stop(false);
-            allgather(c, c.vbuf, c.Bn);
+            exchange(cs, [](Ctx& c) { return c.vbuf; }, c0.Bn);
         }
         // writeback of the column pair (ccd.hpp:209, :226); the residual part is deferred
-        CUDA_TRY(cudaMemcpyAsync(Wt, c.ubuf, sizeof(float) * c.ext_m, cudaMemcpyDeviceToDevice, c.stream));
-        CUDA_TRY(cudaMemcpyAsync(Ht, c.vbuf, sizeof(float) * c.ext_n, cudaMemcpyDeviceToDevice, c.stream));
+        for (Ctx* cp : cs) {
+            Ctx& c = *cp;
+            CUDA_TRY(cudaMemcpyAsync(c.W + static_cast<int64_t>(t) * c.ldm, c.ubuf, sizeof(float) * c.ext_m,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+            CUDA_TRY(cudaMemcpyAsync(c.H + static_cast<int64_t>(t) * c.ldn, c.vbuf, sizeof(float) * c.ext_n,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+        }
     }
+    join_ranks(cs);
     CUDA_TRY(cudaGetLastError());
     return launched;
 }
 
-void ccd_begin(Ctx& c, const pmf_ccd_config* cfg) {
+void check_ccd_config(const pmf_ccd_config* cfg) {
     if (!cfg) invalid("config is null");
     // ccd.hpp:43-49
     if (cfg->k < 1) invalid("k must be >= 1");
     if (cfg->lambda < 0.f) invalid("lambda must be >= 0");
     if (cfg->outer_iters < 1) invalid("outer_iters must be >= 1");
     if (cfg->inner_iters < 1) invalid("inner_iters must be >= 1");
-    CUDA_TRY(cudaSetDevice(c.device));
-    alloc_ccd_model(c, cfg->k);
-    c.mode = 1;
-    c.lambda = cfg->lambda;
-    c.inner = cfg->inner_iters;
-    const auto H = init_items_host(c.n, cfg->k, cfg->seed);
-    upload_colmajor(c, c.H, c.ldn, H.data(), c.n, cfg->k, false);
-    reset_residual(c);
-    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (cfg->num_gpus < 1) invalid("workers must be >= 1");
+}
+
+void ccd_begin(Ctx& c0, const pmf_ccd_config* cfg) {
+    check_ccd_config(cfg);
+    const auto H = init_items_host(c0.n, cfg->k, cfg->seed);  // model.hpp:86-93, replicated
+    for (Ctx* cp : ranks_of(c0)) {
+        Ctx& c = *cp;
+        CUDA_TRY(cudaSetDevice(c.device));
+        alloc_ccd_model(c, cfg->k);
+        c.mode = 1;
+        c.lambda = cfg->lambda;
+        c.inner = cfg->inner_iters;
+        upload_colmajor(c, c.H, c.ldn, H.data(), c.n, cfg->k, false);
+        reset_residual(c);
+        CUDA_TRY(cudaStreamSynchronize(c.stream));
+    }
 }
 
 void ccd_iterate(Ctx& c, int n_outer, double* secs) {
     if (c.mode != 1) invalid("ccdpp_begin has not been called");
     CUDA_TRY(cudaSetDevice(c.device));
-    if (c.profiling) {
+    const Ranks cs = ranks_of(c);
+    const bool graph = !c.profiling && capturable(cs);
+    if (!graph) {
         reset_graph(c);
         c.stat_u_ms = c.stat_v_ms = 0;
         c.stat_u_n = c.stat_v_n = 0;
@@ -835,7 +896,7 @@ void ccd_iterate(Ctx& c, int n_outer, double* secs) {
         CUDA_TRY(cudaStreamBeginCapture(c.stream, cudaStreamCaptureModeThreadLocal));
         int64_t launched = 0;
         try {
-            launched = enqueue_ccd_iteration(c);
+            launched = enqueue_ccd_iteration(cs);
         } catch (...) {
             cudaGraph_t g;
             cudaStreamEndCapture(c.stream, &g);
@@ -851,7 +912,7 @@ void ccd_iterate(Ctx& c, int n_outer, double* secs) {
     CUDA_TRY(cudaEventCreate(&e1));
     for (int it = 0; it < n_outer; ++it) {
         CUDA_TRY(cudaEventRecord(e0, c.stream));
-        if (c.profiling) c.launches_per_iter = enqueue_ccd_iteration(c);
+        if (!graph) c.launches_per_iter = enqueue_ccd_iteration(cs);
         else CUDA_TRY(cudaGraphLaunch(c.graph_exec, c.stream));
         CUDA_TRY(cudaEventRecord(e1, c.stream));
         CUDA_TRY(cudaEventSynchronize(e1));
@@ -917,6 +978,39 @@ void build_als(Ctx& c, const pmf_matrix_view* a) {
     c.als_built = true;
 }
 
+// A device group of `world` ranks in this process: rank r owns CSR row block r and CSC column block r
+// (the multi-process plan, runtime.hpp:91-136) on devices[r] (default: device r mod the device
+// count, so a 1-GPU host runs a group as loopback ranks on one device).  Returns rank 0.
+std::unique_ptr<Ctx> make_group(const pmf_matrix_view* a, int world, const int32_t* devices, bool als) {
+    if (world < 1) invalid("workers must be >= 1");
+    ensure_device();
+    int ndev = 0;
+    CUDA_TRY(cudaGetDeviceCount(&ndev));
+    std::vector<std::unique_ptr<Ctx>> rs;
+    for (int r = 0; r < world; ++r) {
+        const int dev = devices ? devices[r] : r % ndev;
+        if (dev < 0 || dev >= ndev) invalid("device index out of range");
+        rs.push_back(make_ctx(a, dev, r, world, nullptr));
+        if (als) build_als(*rs.back(), a);
+    }
+    for (int r = 0; r < world; ++r)
+        for (int q = 0; q < world; ++q) {
+            const int dr = rs[r]->device, dq = rs[q]->device;
+            int ok = 0;
+            if (dr == dq || cudaDeviceCanAccessPeer(&ok, dr, dq) != cudaSuccess || !ok) continue;
+            CUDA_TRY(cudaSetDevice(dr));
+            if (cudaDeviceEnablePeerAccess(dq, 0) != cudaSuccess) cudaGetLastError();  // already enabled
+        }
+    std::unique_ptr<Ctx> c0 = std::move(rs[0]);
+    c0->ranks.push_back(c0.get());
+    for (int r = 1; r < world; ++r) {
+        c0->ranks.push_back(rs[r].get());
+        c0->peers.push_back(std::move(rs[r]));
+    }
+    CUDA_TRY(cudaSetDevice(c0->device));
+    return c0;
+}
+
 void als_alloc_partials(Ctx& c, int k) {
     // partial buffers depend on k; (re)allocate in model_mem
     const int64_t stride = static_cast<int64_t>(k) * k + k + 1;
@@ -924,59 +1018,70 @@ void als_alloc_partials(Ctx& c, int k) {
     c.als_csc.partial = c.model_mem.alloc<float>(std::max<int64_t>(1, c.als_csc.n_slots * stride), false);
 }
 
-void als_begin(Ctx& c, const pmf_als_config* cfg) {
+void als_begin(Ctx& c0, const pmf_als_config* cfg) {
     if (!cfg) invalid("config is null");
     // als.hpp:34-39
     if (cfg->k < 1) invalid("k must be >= 1");
     if (!(cfg->lambda > 0.f)) invalid("als requires lambda > 0");
     if (cfg->outer_iters < 1) invalid("outer_iters must be >= 1");
+    if (cfg->num_gpus < 1) invalid("workers must be >= 1");
     if (cfg->k > 64) invalid("the B200 ALS kernels support k <= 64");
-    if (!c.als_built) invalid("context was created without ALS layouts");
-    CUDA_TRY(cudaSetDevice(c.device));
-    reset_graph(c);
-    c.model_mem.free_all();
-    c.k = cfg->k;
-    c.lambda = cfg->lambda;
-    c.als_weighted = (cfg->flags & PMF_ALS_WEIGHTED_LAMBDA) != 0;
-    c.ccdw_on = false;
-    c.W = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_m + 1) * c.k);
-    c.H = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_n + 1) * c.k);
-    als_alloc_partials(c, c.k);
-    const auto H = init_items_host(c.n, cfg->k, cfg->seed);
-    upload_rowmajor(c, c.H, c.ext_n, H.data(), c.n, cfg->k, false);
-    c.mode = 2;
+    if (!c0.als_built) invalid("context was created without ALS layouts");
+    const auto H = init_items_host(c0.n, cfg->k, cfg->seed);  // model.hpp:86-93, replicated
+    for (Ctx* cp : ranks_of(c0)) {
+        Ctx& c = *cp;
+        CUDA_TRY(cudaSetDevice(c.device));
+        reset_graph(c);
+        c.model_mem.free_all();
+        c.k = cfg->k;
+        c.lambda = cfg->lambda;
+        c.als_weighted = (cfg->flags & PMF_ALS_WEIGHTED_LAMBDA) != 0;
+        c.ccdw_on = false;
+        c.W = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_m + 1) * c.k);
+        c.H = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_n + 1) * c.k);
+        als_alloc_partials(c, c.k);
+        upload_rowmajor(c, c.H, c.ext_n, H.data(), c.n, cfg->k, false);
+        c.mode = 2;
+    }
 }
 
-int64_t enqueue_als_iteration(Ctx& c) {
+int64_t enqueue_als_iteration(const Ranks& cs) {
     int64_t launched = 0;
+    fork_ranks(cs);
     // W phase from the old H, then H phase from the new W (als.hpp:176-184)
-    launched += launch_als_half(c.als_csr, c.H, c.ext_n, c.W, c.rank * c.Bm, c.k, c.lambda, c.als_weighted,
-                                c.d_counter, c.d_status, c.sm_count, c.stream);
-    allgather(c, c.W, static_cast<int64_t>(c.Bm) * c.k);
-    launched += launch_als_half(c.als_csc, c.W, c.ext_m, c.H, c.rank * c.Bn, c.k, c.lambda, c.als_weighted,
-                                c.d_counter + 1, c.d_status, c.sm_count, c.stream);
-    allgather(c, c.H, static_cast<int64_t>(c.Bn) * c.k);
+    for (Ctx* c : cs)
+        launched += launch_als_half(c->als_csr, c->H, c->ext_n, c->W, c->rank * c->Bm, c->k, c->lambda,
+                                    c->als_weighted, c->d_counter, c->d_status, c->sm_count, c->stream);
+    exchange(cs, [](Ctx& c) { return c.W; }, static_cast<int64_t>(cs[0]->Bm) * cs[0]->k);
+    for (Ctx* c : cs)
+        launched += launch_als_half(c->als_csc, c->W, c->ext_m, c->H, c->rank * c->Bn, c->k, c->lambda,
+                                    c->als_weighted, c->d_counter + 1, c->d_status, c->sm_count, c->stream);
+    exchange(cs, [](Ctx& c) { return c.H; }, static_cast<int64_t>(cs[0]->Bn) * cs[0]->k);
+    join_ranks(cs);
     return launched;
 }
 
 void als_iterate(Ctx& c, int n_outer, double* secs) {
     if (c.mode != 2 || c.ccdw_on) invalid("als_begin has not been called");
     CUDA_TRY(cudaSetDevice(c.device));
+    const Ranks cs = ranks_of(c);
     cudaEvent_t e0, e1;
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
     for (int it = 0; it < n_outer; ++it) {
-        CUDA_TRY(cudaMemsetAsync(c.d_status, 0, sizeof(int), c.stream));
+        for (Ctx* r : cs) CUDA_TRY(cudaMemsetAsync(r->d_status, 0, sizeof(int), r->stream));
         CUDA_TRY(cudaEventRecord(e0, c.stream));
-        c.launches_per_iter = enqueue_als_iteration(c);
+        c.launches_per_iter = enqueue_als_iteration(cs);
         CUDA_TRY(cudaEventRecord(e1, c.stream));
         CUDA_TRY(cudaEventSynchronize(e1));
         float ms = 0;
         CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
         if (secs) secs[it] = ms * 1e-3;
-        int st = 0;
-        CUDA_TRY(cudaMemcpy(&st, c.d_status, sizeof(int), cudaMemcpyDeviceToHost));
-        if (st == 4) throw PmfError(PMF_NOT_POSITIVE_DEFINITE, "non-positive pivot in an ALS row solve");
+        for (Ctx* r : cs) {
+            int st = 0;
+            CUDA_TRY(cudaMemcpy(&st, r->d_status, sizeof(int), cudaMemcpyDeviceToHost));
+            if (st == 4) throw PmfError(PMF_NOT_POSITIVE_DEFINITE, "non-positive pivot in an ALS row solve");
+        }
     }
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
@@ -991,6 +1096,7 @@ void ccdw_begin(Ctx& c, const pmf_ccd_config* cfg) {
     if (cfg->lambda < 0.f) invalid("lambda must be >= 0");
     if (cfg->outer_iters < 1) invalid("outer_iters must be >= 1");
     if (cfg->inner_iters < 1) invalid("inner_iters must be >= 1");
+    if (cfg->num_gpus < 1) invalid("workers must be >= 1");
     if (c.world != 1) invalid("item/user-wise CCD runs on one device (ccd.hpp:306-309)");
     if (!c.als_built) invalid("context was created without the plain CSR / CSC layouts");
     if (c.nnz >= (int64_t(1) << 31)) invalid("item/user-wise CCD: more than 2^31 - 1 ratings");
@@ -1086,8 +1192,9 @@ FactorView hview(const Ctx& c) {
     return FactorView{c.H, c.k, 1};
 }
 
-void metrics(Ctx& c, double* objective, double* rmse, double* train_rmse) {
-    if (c.mode == 0) invalid("no model: call ccdpp_begin or als_begin first");
+// Enqueues this rank's metric terms into c.red_out: [0] its CSR block's squared error, [1] |W|^2,
+// [2] |H|^2, [3] the probe SSE (the last three over the replicated model).
+void enqueue_metric_terms(Ctx& c) {
     CUDA_TRY(cudaSetDevice(c.device));
     FactorView W = wview(c), H = hview(c);
     if (c.mode == 1) {
@@ -1113,16 +1220,29 @@ void metrics(Ctx& c, double* objective, double* rmse, double* train_rmse) {
     launch_sumsq(c.H, hn, c.red_scratch + 2048, c.red_out + 2, c.stream);
     if (c.n_probe > 0) launch_probe_sse(c.probe, c.n_probe, W, H, c.k, c.red_scratch + 3072, c.red_out + 3, c.stream);
     if (c.comm) NCCL_TRY(ncclAllReduce(c.red_out, c.red_out, 1, ncclDouble, ncclSum, c.comm, c.stream));
+}
+
+void metrics(Ctx& c, double* objective, double* rmse, double* train_rmse) {
+    if (c.mode == 0) invalid("no model: call ccdpp_begin or als_begin first");
+    const Ranks cs = ranks_of(c);
+    for (Ctx* r : cs) enqueue_metric_terms(*r);
     double h[4] = {0, 0, 0, 0};
-    CUDA_TRY(cudaMemcpyAsync(h, c.red_out, sizeof(h), cudaMemcpyDeviceToHost, c.stream));
-    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    for (Ctx* r : cs) {  // a group's squared error: its row blocks' sums in rank order
+        double t[4];
+        CUDA_TRY(cudaSetDevice(r->device));
+        CUDA_TRY(cudaMemcpyAsync(t, r->red_out, sizeof(t), cudaMemcpyDeviceToHost, r->stream));
+        CUDA_TRY(cudaStreamSynchronize(r->stream));
+        h[0] += t[0];
+        if (r == cs[0]) std::copy(t + 1, t + 4, h + 1);
+    }
+    CUDA_TRY(cudaSetDevice(c.device));
     const double lam = static_cast<double>(c.lambda);  // Real lambda widened (ccd.hpp:394)
     if (objective) *objective = h[0] + lam * (h[1] + h[2]);
     if (train_rmse) *train_rmse = c.nnz > 0 ? std::sqrt(h[0] / static_cast<double>(c.nnz)) : 0.0;
     if (rmse) *rmse = c.n_probe > 0 ? std::sqrt(h[3] / static_cast<double>(c.n_probe)) : std::nan("");
 }
 
-void set_probe(Ctx& c, const pmf_triplet* probe, int64_t n) {
+void set_probe_one(Ctx& c, const pmf_triplet* probe, int64_t n) {
     if (n < 0 || (n > 0 && !probe)) invalid("probe is null");
     for (int64_t x = 0; x < n; ++x)
         if (probe[x].user < 0 || probe[x].user >= c.m || probe[x].item < 0 || probe[x].item >= c.n)
@@ -1136,6 +1256,9 @@ void set_probe(Ctx& c, const pmf_triplet* probe, int64_t n) {
     for (int64_t x = 0; x < n; ++x) t[x] = DevTriplet{c.prow(probe[x].user), c.pcol(probe[x].item), probe[x].rating};
     c.probe = c.probe_mem.upload(t, c.stream, &c.h2d);
     CUDA_TRY(cudaStreamSynchronize(c.stream));
+}
+void set_probe(Ctx& c, const pmf_triplet* probe, int64_t n) {
+    for (Ctx* r : ranks_of(c)) set_probe_one(*r, probe, n);
 }
 
 void get_model(Ctx& c, float* W, float* H) {
@@ -1183,16 +1306,37 @@ void get_model(Ctx& c, float* W, float* H) {
     }
 }
 
-void set_model(Ctx& c, const float* W, const float* H, int k) {
+// Installs a model.  The residual solvers' state follows it: CCD++ gets R = A - W H^T in the
+// deferred form its first sweep expects (column k-1's product still to be subtracted, so the next
+// sweep completes A - sum_t w_t h_t in ascending t), item/user-wise CCD R = A - W H^T in both layouts.
+void set_model_one(Ctx& c, const float* W, const float* H, int k, bool residual) {
     if (c.mode == 0) invalid("no model: call ccdpp_begin or als_begin first");
     if (k != c.k) invalid("rank does not match the active model");
+    if (!W || !H) invalid("null buffers");
+    CUDA_TRY(cudaSetDevice(c.device));
     if (c.mode == 1) {
         upload_colmajor(c, c.W, c.ldm, W, c.m, k, true);
         upload_colmajor(c, c.H, c.ldn, H, c.n, k, false);
+        if (residual) reset_residual(c);
+        for (int t = 0; residual && t + 1 < k; ++t) {
+            SweepOperands o1, o2;
+            o1.oa = c.W + static_cast<int64_t>(t) * c.ldm;
+            o1.ga = c.H + static_cast<int64_t>(t) * c.ldn;
+            o2.oa = c.H + static_cast<int64_t>(t) * c.ldn;
+            o2.ga = c.W + static_cast<int64_t>(t) * c.ldm;
+            launch_sweep(c.csr, kDemote, true, o1, c.stream);
+            launch_sweep(c.csc, kDemote, false, o2, c.stream);
+        }
     } else {
         upload_rowmajor(c, c.W, c.ext_m, W, c.m, k, true);
         upload_rowmajor(c, c.H, c.ext_n, H, c.n, k, false);
+        if (c.ccdw_on && !c.ccdw_gram) launch_ccd_residual(c.ccdw, c.als_csr.val, c.W, c.H, k, c.stream);
     }
+    CUDA_TRY(cudaStreamSynchronize(c.stream));
+    CUDA_TRY(cudaGetLastError());
+}
+void set_model(Ctx& c, const float* W, const float* H, int k, bool residual = true) {
+    for (Ctx* r : ranks_of(c)) set_model_one(*r, W, H, k, residual);
 }
 
 // host scatter/gather between reference order and the padded layout
@@ -1282,6 +1426,14 @@ pmf_status pmf_ctx_create_dist(const pmf_matrix_view* a, int32_t device, int32_t
         if (!id) invalid("nccl id is null");
         auto c = make_ctx(a, device, rank, world, id);
         build_als(*c, a);
+        *out = reinterpret_cast<pmf_ctx*>(c.release());
+    });
+}
+
+pmf_status pmf_ctx_create_group(const pmf_matrix_view* a, int32_t num_gpus, const int32_t* devices, pmf_ctx** out) {
+    return guard([&] {
+        if (!out) invalid("out is null");
+        auto c = make_group(a, num_gpus, devices, true);
         *out = reinterpret_cast<pmf_ctx*>(c.release());
     });
 }
@@ -1506,10 +1658,11 @@ pmf_status pmf_top_n(const float* W, const float* H, int32_t m, int32_t n, int32
             for (int64_t p = ex_start[u] + 1; p < ex_start[u + 1]; ++p)
                 if (ex_items[p] <= ex_items[p - 1]) invalid("rated items must be strictly increasing");
         }
+        // the tiled kernel keeps each user's list in shared memory; larger k x count take the wide
+        // path (full scoring + segmented sort), with the same results
         const size_t smem = topn_smem_bytes(k, count);
         constexpr size_t kTopnSmemMax = 224 * 1024;  // + the kernel's static shared memory <= 227 KB
-        if (smem > kTopnSmemMax) invalid("top_n on the GPU: k x count too large for shared memory (k " +
-                                       std::to_string(k) + ", count " + std::to_string(count) + ")");
+        const bool wide = smem > kTopnSmemMax;
         if (n_users == 0) return;
         ensure_device();
         static bool attr = false;
@@ -1542,7 +1695,13 @@ pmf_status pmf_top_n(const float* W, const float* H, int32_t m, int32_t n, int32
         CUDA_TRY(cudaEventCreate(&e0));
         CUDA_TRY(cudaEventCreate(&e1));
         CUDA_TRY(cudaEventRecord(e0, s));
-        launch_topn(dW, dH, n, k, du, n_users, des, dex, count, doi, dos, doc, s);
+        if (wide) {
+            const int batch = std::min(topn_wide_batch(n), n_users);
+            void* scratch = mem.alloc<char>(topn_wide_scratch_bytes(n, batch), false);
+            CUDA_TRY(launch_topn_wide(dW, dH, n, k, du, n_users, des, dex, count, doi, dos, doc, scratch, batch, s));
+        } else {
+            launch_topn(dW, dH, n, k, du, n_users, des, dex, count, doi, dos, doc, s);
+        }
         CUDA_TRY(cudaEventRecord(e1, s));
         CUDA_TRY(cudaGetLastError());
         if (std::getenv("PMF_VERBOSE")) {
@@ -1583,9 +1742,9 @@ pmf_status pmf_ctx_layout_info(pmf_ctx* ctx, int32_t side, pmf_layout_info* out)
 }  // extern "C"
 
 template <class Begin, class Iterate>
-static pmf_status train_common(const pmf_matrix_view* a, int outer, const pmf_triplet* probe, int64_t n_probe,
-                               float* W_out, float* H_out, pmf_iter_row* rows, pmf_train_totals* totals,
-                               Begin begin, Iterate iterate) {
+static pmf_status train_common(const pmf_matrix_view* a, int outer, int world, bool als, const pmf_triplet* probe,
+                               int64_t n_probe, float* W_out, float* H_out, pmf_iter_row* rows,
+                               pmf_train_totals* totals, Begin begin, Iterate iterate) {
     return guard([&] {
         const double t0 = now_s();
         if (!rows) invalid("rows_out is null");
@@ -1595,7 +1754,9 @@ static pmf_status train_common(const pmf_matrix_view* a, int outer, const pmf_tr
             if (probe[x].user < 0 || probe[x].user >= a->m || probe[x].item < 0 || probe[x].item >= a->n)
                 invalid("probe index outside training dimensions");
         const double t_val = now_s();
-        auto c = make_ctx(a, -1, 0, 1, nullptr);
+        if (world < 1) invalid("workers must be >= 1");
+        auto c = world == 1 ? make_ctx(a, -1, 0, 1, nullptr) : make_group(a, world, nullptr, als);
+        if (world == 1 && als) build_als(*c, a);
         const double t_ctx = now_s();
         begin(*c);
         set_probe(*c, probe, n_probe);
@@ -1625,9 +1786,12 @@ static pmf_status train_common(const pmf_matrix_view* a, int outer, const pmf_tr
             totals->train_seconds = train;
             totals->final_objective = rows[outer - 1].objective;
             totals->final_rmse = rows[outer - 1].rmse;
-            totals->setup_seconds = c->setup_seconds;
-            totals->h2d_bytes = c->h2d;
-            totals->d2h_bytes = c->d2h;
+            totals->setup_seconds = world == 1 ? c->setup_seconds : t_ctx - t_val;
+            totals->h2d_bytes = totals->d2h_bytes = 0;
+            for (Ctx* r : ranks_of(*c)) {
+                totals->h2d_bytes += r->h2d;
+                totals->d2h_bytes += r->d2h;
+            }
             totals->kernel_launches = c->launches_per_iter * outer;
             totals->wall_seconds = now_s() - t0;
         }
@@ -1639,13 +1803,11 @@ extern "C" {
 pmf_status pmf_ccdpp_train(const pmf_ccd_config* cfg, const pmf_matrix_view* a, const pmf_triplet* probe,
                            int64_t n_probe, float* W_out, float* H_out, pmf_iter_row* rows,
                            pmf_train_totals* totals) {
-    if (!cfg) {
-        g_err = "config is null";
-        return PMF_INVALID_ARGUMENT;
-    }
+    if (const pmf_status st = guard([&] { check_ccd_config(cfg); }); st != PMF_OK) return st;
+    // ccd.hpp:39 `workers` -> GPUs: a device group of num_gpus ranks
     return train_common(
-        a, cfg->outer_iters, probe, n_probe, W_out, H_out, rows, totals, [&](Ctx& c) { ccd_begin(c, cfg); },
-        [&](Ctx& c, double* s) { ccd_iterate(c, 1, s); });
+        a, cfg->outer_iters, cfg->num_gpus, false, probe, n_probe, W_out, H_out, rows, totals,
+        [&](Ctx& c) { ccd_begin(c, cfg); }, [&](Ctx& c, double* s) { ccd_iterate(c, 1, s); });
 }
 
 pmf_status pmf_ccd_train(const pmf_ccd_config* cfg, const pmf_matrix_view* a, const pmf_triplet* probe,
@@ -1654,10 +1816,14 @@ pmf_status pmf_ccd_train(const pmf_ccd_config* cfg, const pmf_matrix_view* a, co
         g_err = "config is null";
         return PMF_INVALID_ARGUMENT;
     }
+    // ccd_train runs one worker whatever `workers` says (ccd.hpp:306-309): one device
+    if (cfg->num_gpus < 1) {
+        g_err = "workers must be >= 1";
+        return PMF_INVALID_ARGUMENT;
+    }
     return train_common(
-        a, cfg->outer_iters, probe, n_probe, W_out, H_out, rows, totals,
+        a, cfg->outer_iters, 1, true, probe, n_probe, W_out, H_out, rows, totals,
         [&](Ctx& c) {
-            build_als(c, a);
             ccdw_begin(c, cfg);
         },
         [&](Ctx& c, double* s) { ccdw_iterate(c, 1, s); });
@@ -1669,14 +1835,16 @@ pmf_status pmf_als_train(const pmf_als_config* cfg, const pmf_matrix_view* a, co
         g_err = "config is null";
         return PMF_INVALID_ARGUMENT;
     }
-    if (cfg->outer_iters < 1 || cfg->k < 1 || !(cfg->lambda > 0.f)) {
-        g_err = cfg->outer_iters < 1 ? "outer_iters must be >= 1" : cfg->k < 1 ? "k must be >= 1" : "als requires lambda > 0";
+    if (cfg->outer_iters < 1 || cfg->k < 1 || !(cfg->lambda > 0.f) || cfg->num_gpus < 1) {
+        g_err = cfg->outer_iters < 1 ? "outer_iters must be >= 1"
+                : cfg->k < 1         ? "k must be >= 1"
+                : cfg->num_gpus < 1  ? "workers must be >= 1"
+                                     : "als requires lambda > 0";
         return PMF_INVALID_ARGUMENT;
     }
     return train_common(
-        a, cfg->outer_iters, probe, n_probe, W_out, H_out, rows, totals,
+        a, cfg->outer_iters, cfg->num_gpus, true, probe, n_probe, W_out, H_out, rows, totals,
         [&](Ctx& c) {
-            build_als(c, a);
             als_begin(c, cfg);
         },
         [&](Ctx& c, double* s) { als_iterate(c, 1, s); });
@@ -1722,7 +1890,7 @@ pmf_status pmf_objective(const pmf_matrix_view* a, const float* W, const float* 
         auto c = make_ctx(a, -1, 0, 1, nullptr);
         alloc_ccd_model(*c, k);
         c->mode = 1;
-        set_model(*c, W, H, k);
+        set_model(*c, W, H, k, false);
         c->lambda = 0.f;
         double obj = 0;
         metrics(*c, &obj, nullptr, nullptr);

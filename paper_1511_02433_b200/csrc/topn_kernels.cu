@@ -13,6 +13,9 @@
 // current last entry; insertions are warp-cooperative (position by ballot, then shift).
 #include <cuda_runtime.h>
 
+#include <cub/device/device_segmented_radix_sort.cuh>
+
+#include <algorithm>
 #include <cfloat>
 #include <cstdint>
 
@@ -187,7 +190,155 @@ topn_kernel(const float* __restrict__ W, const float* __restrict__ H, int32_t n,
     if (threadIdx.x < nu) out_count[u0 + threadIdx.x] = s_filled[threadIdx.x];
 }
 
+// ---- wide path: any count / any k (model.hpp:172-209 accepts both) -------------------------------
+// A batch of users at a time: every item scored with predict()'s roundings, rated items' sort keys
+// forced below every score, then one stable segmented radix sort (descending) per user over
+// order-preserving keys -- -0 is keyed as +0, so equal scores keep ascending item order exactly as
+// the reference's comparator (a.second != b.second ? a.second > b.second : a.first < b.first).
+
+__device__ __forceinline__ uint32_t score_key(float s) {
+    const uint32_t b = s == 0.f ? 0u : __float_as_uint(s);  // -0 == +0
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
+__global__ void topn_score_kernel(const float* __restrict__ W, const float* __restrict__ H, int32_t n, int k,
+                                  const int32_t* __restrict__ users, float* __restrict__ scores,
+                                  uint32_t* __restrict__ keys, int32_t* __restrict__ items) {
+    const int32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= n) return;
+    const int b = blockIdx.y;
+    const float* w = W + static_cast<int64_t>(users[b]) * k;
+    const float* h = H + static_cast<int64_t>(j) * k;
+    float acc = 0.f;
+    for (int t = 0; t < k; ++t) acc = __fadd_rn(acc, __fmul_rn(w[t], h[t]));
+    const int64_t o = static_cast<int64_t>(b) * n + j;
+    scores[o] = acc;
+    keys[o] = score_key(acc);
+    items[o] = j;
+}
+
+__global__ void topn_exclude_kernel(const int64_t* __restrict__ ex_start, const int32_t* __restrict__ ex_items,
+                                    int32_t n, uint32_t* __restrict__ keys, int32_t* __restrict__ excluded,
+                                    int32_t* __restrict__ seg) {
+    const int b = blockIdx.x;
+    __shared__ int cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    int mine = 0;
+    for (int64_t p = ex_start[b] + threadIdx.x; p < ex_start[b + 1]; p += blockDim.x) {
+        const int32_t j = ex_items[p];
+        if (j >= 0 && j < n) {
+            keys[static_cast<int64_t>(b) * n + j] = 0u;  // below every score key
+            ++mine;
+        }
+    }
+    atomicAdd(&cnt, mine);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        excluded[b] = cnt;
+        seg[b] = b * n;
+        if (b == gridDim.x - 1) seg[b + 1] = (b + 1) * n;
+    }
+}
+
+__global__ void topn_emit_kernel(const float* __restrict__ scores, const int32_t* __restrict__ sorted_items,
+                                 const int32_t* __restrict__ excluded, int32_t n, int count,
+                                 int32_t* __restrict__ out_items, float* __restrict__ out_scores,
+                                 int32_t* __restrict__ out_count) {
+    const int b = blockIdx.x;
+    const int keep = min(count, n - excluded[b]);
+    for (int r = threadIdx.x; r < count; r += blockDim.x) {
+        const int64_t o = static_cast<int64_t>(b) * count + r;
+        if (r < keep) {
+            const int32_t j = sorted_items[static_cast<int64_t>(b) * n + r];
+            out_items[o] = j;
+            out_scores[o] = scores[static_cast<int64_t>(b) * n + j];
+        } else {
+            out_items[o] = -1;
+            out_scores[o] = 0.f;
+        }
+    }
+    if (threadIdx.x == 0) out_count[b] = keep;
+}
+
+struct WideScratch {
+    float* scores;
+    uint32_t *keys, *keys_out;
+    int32_t *items, *items_out, *excluded, *seg;
+    void* temp;
+    size_t temp_bytes;
+};
+
+WideScratch carve(void* base, int32_t n, int batch, size_t temp_bytes) {
+    auto* p = static_cast<char*>(base);
+    const size_t e = static_cast<size_t>(batch) * n;
+    auto take = [&](size_t bytes) {
+        char* q = p;
+        p += (bytes + 255) & ~size_t(255);
+        return q;
+    };
+    WideScratch w;
+    w.scores = reinterpret_cast<float*>(take(e * 4));
+    w.keys = reinterpret_cast<uint32_t*>(take(e * 4));
+    w.keys_out = reinterpret_cast<uint32_t*>(take(e * 4));
+    w.items = reinterpret_cast<int32_t*>(take(e * 4));
+    w.items_out = reinterpret_cast<int32_t*>(take(e * 4));
+    w.excluded = reinterpret_cast<int32_t*>(take(static_cast<size_t>(batch) * 4));
+    w.seg = reinterpret_cast<int32_t*>(take((static_cast<size_t>(batch) + 1) * 4));
+    w.temp = take(temp_bytes);
+    w.temp_bytes = temp_bytes;
+    return w;
+}
+
+size_t sort_temp_bytes(int32_t n, int batch) {
+    size_t bytes = 0;
+    cub::DeviceSegmentedRadixSort::SortPairsDescending(nullptr, bytes, static_cast<const uint32_t*>(nullptr),
+                                                       static_cast<uint32_t*>(nullptr),
+                                                       static_cast<const int32_t*>(nullptr),
+                                                       static_cast<int32_t*>(nullptr), batch * n, batch,
+                                                       static_cast<const int32_t*>(nullptr),
+                                                       static_cast<const int32_t*>(nullptr));
+    return bytes;
+}
+
 }  // namespace
+
+int topn_wide_batch(int32_t n) {
+    const int64_t per_user = std::max<int64_t>(1, 24 * static_cast<int64_t>(n));
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(4096, (int64_t(768) << 20) / per_user)));
+}
+
+size_t topn_wide_scratch_bytes(int32_t n, int batch) {
+    const size_t e = static_cast<size_t>(batch) * std::max(n, 1);
+    return 5 * ((e * 4 + 255) & ~size_t(255)) + 2 * 256 + static_cast<size_t>(batch + 1) * 8 +
+           sort_temp_bytes(std::max(n, 1), batch) + 256;
+}
+
+cudaError_t launch_topn_wide(const float* W, const float* H, int32_t n, int k, const int32_t* users, int32_t n_users,
+                             const int64_t* ex_start, const int32_t* ex_items, int count, int32_t* out_items,
+                             float* out_scores, int32_t* out_count, void* scratch, int batch, cudaStream_t s) {
+    if (n_users <= 0) return cudaSuccess;
+    if (n <= 0) {  // nothing to rank: every list is empty
+        cudaMemsetAsync(out_count, 0, sizeof(int32_t) * n_users, s);
+        cudaMemsetAsync(out_scores, 0, sizeof(float) * static_cast<size_t>(n_users) * count, s);
+        return cudaMemsetAsync(out_items, 0xff, sizeof(int32_t) * static_cast<size_t>(n_users) * count, s);
+    }
+    const size_t tb = sort_temp_bytes(n, batch);
+    WideScratch w = carve(scratch, n, batch, tb);
+    for (int32_t u0 = 0; u0 < n_users; u0 += batch) {
+        const int B = std::min<int32_t>(batch, n_users - u0);
+        topn_score_kernel<<<dim3((n + 255) / 256, B), 256, 0, s>>>(W, H, n, k, users + u0, w.scores, w.keys, w.items);
+        topn_exclude_kernel<<<B, 256, 0, s>>>(ex_start + u0, ex_items, n, w.keys, w.excluded, w.seg);
+        size_t bytes = w.temp_bytes;
+        const cudaError_t e = cub::DeviceSegmentedRadixSort::SortPairsDescending(
+            w.temp, bytes, w.keys, w.keys_out, w.items, w.items_out, B * n, B, w.seg, w.seg + 1, 0, 32, s);
+        if (e != cudaSuccess) return e;
+        topn_emit_kernel<<<B, 256, 0, s>>>(w.scores, w.items_out, w.excluded, n, count,
+                                           out_items + static_cast<int64_t>(u0) * count,
+                                           out_scores + static_cast<int64_t>(u0) * count, out_count + u0);
+    }
+    return cudaGetLastError();
+}
 
 size_t topn_smem_bytes(int k, int count) {
     return static_cast<size_t>(k) * (kTnTile + 4) * sizeof(float) + static_cast<size_t>(k) * kTnUsers * sizeof(float) +

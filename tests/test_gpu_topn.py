@@ -45,6 +45,22 @@ def test_topn_random_vs_oracle(pmf, oracle, m, n, k, count):
     _check_batch(pmf, oracle, W, H, users, count, rated)
 
 
+@pytest.mark.parametrize("m,n,k,count", [(40, 300, 10, 300), (30, 257, 10, 1000), (20, 900, 100, 400),
+                                         (12, 500, 200, 7), (9, 64, 3, 64)])
+def test_topn_wide_vs_oracle(pmf, oracle, m, n, k, count):
+    """count >= items (every unrated item ranked) and k x count past the tiled kernel's shared memory:
+    the wide path (full scoring + stable segmented sort), same results."""
+    rng = np.random.default_rng(m * n + k)
+    W = rng.uniform(-1, 1, (m, k)).astype(np.float32)
+    H = rng.uniform(-1, 1, (n, k)).astype(np.float32)
+    H[::4] = np.round(H[::4] * 2) / 2
+    W[::3] = np.round(W[::3] * 2) / 2
+    W[1] = 0.0                                   # +0 / -0 scores: ties by ascending item
+    users = np.arange(m, dtype=np.int32)
+    rated = [np.sort(rng.choice(n, rng.integers(0, n // 2), replace=False)).astype(np.int32) for _ in users]
+    _check_batch(pmf, oracle, W, H, users, count, rated)
+
+
 def test_topn_matrix_exclusion_vs_oracle(pmf, oracle, ml100k):
     train, _ = ml100k
     A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
