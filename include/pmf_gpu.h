@@ -245,15 +245,6 @@ pmf_status pmf_matrix_from_triplets(const pmf_triplet* t, int64_t nnz, int32_t m
 pmf_status pmf_matrix_from_triplets_gpu(const pmf_triplet* t, int64_t nnz, int32_t m, int32_t n,
                                         int64_t* row_start, int32_t* col_of, float* val_row,
                                         int64_t* col_start, int32_t* row_of, float* val_col);
-/* Synthetic ratings with the recipe of tests/testutil.hpp:91-132 (planted rank + biases + noise,
- * 1..5 stars, uniform users, Zipf(0.8) items, no duplicates), generated per user from
- * independent mt19937 streams so it runs in parallel.  Writes `total` = n_train + n_probe
- * triplets sorted by (user, item); probe entries (chosen per user, seeded) are moved to
- * out_probe.  Returns the counts actually produced. */
-pmf_status pmf_synth_ratings(int32_t m, int32_t n, int32_t true_rank, int64_t n_train,
-                             int64_t n_probe, uint32_t seed, pmf_triplet* out_train,
-                             pmf_triplet* out_probe, int64_t* got_train, int64_t* got_probe);
-
 const char* pmf_last_error(void);
 int32_t pmf_abi_version(void);
 int32_t pmf_device_count(void);

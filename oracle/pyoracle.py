@@ -306,11 +306,11 @@ class Reference:
             getattr(L, "ref_ccdpp_train" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, C.c_int, U64,
                                                             P, I64, P, P, P, P]
             getattr(L, "ref_ccdpp_stage_loop" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, C.c_int,
-                                                                 U64, P, I64, P, P, P, P, P]
+                                                                 U64, P, I64, P, P, P, P, P, P, P]
             getattr(L, "ref_als_train" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, U64, P, I64,
                                                           P, P, P, P]
             getattr(L, "ref_als_epochs" + sfx).argtypes = [P, C.c_int, R, C.c_int, C.c_int, U64, P, I64,
-                                                           P, P, P]
+                                                           P, P, P, P, P]
             getattr(L, "ref_ccdpp_update_u" + sfx).argtypes = [P, P, P, P, R]
             getattr(L, "ref_ccdpp_update_v" + sfx).argtypes = [P, P, P, P, R]
             getattr(L, "ref_solve_rows" + sfx).argtypes = [P, C.c_int, P, C.c_int, R, P]
@@ -490,16 +490,19 @@ class RefMatrix:
             self.h, k, lam, outer, seed, ptr(pr), len(pr), ptr(W), ptr(H), ptr(rows)))
         return W, H, rows
 
-    def ccdpp_stage_loop(self, k, lam, outer, inner, seed, probe=None, workers=1):
+    def ccdpp_stage_loop(self, k, lam, outer, inner, seed, probe=None, workers=1, history=False):
+        """history=True: also the model after every outer iteration, (W_hist, H_hist) [outer, rows, k]."""
         dt, _, _ = real_of(self.real)
         pr = self._probe(probe)
         W = np.zeros((self.m, k), dt); H = np.zeros((self.n, k), dt)
         rr = np.zeros(self.nnz, dt); rc = np.zeros(self.nnz, dt)
         rows = np.zeros(outer, ITER_ROW)
+        Wh = np.zeros((outer, self.m, k), dt) if history else None
+        Hh = np.zeros((outer, self.n, k), dt) if history else None
         self.ref._check(getattr(self.ref.lib, "ref_ccdpp_stage_loop" + self.real)(
             self.h, k, lam, outer, inner, workers, seed, ptr(pr), len(pr), ptr(W), ptr(H), ptr(rr), ptr(rc),
-            ptr(rows)))
-        return W, H, rows, rr, rc
+            ptr(rows), ptr(Wh), ptr(Hh)))
+        return (W, H, rows, rr, rc, Wh, Hh) if history else (W, H, rows, rr, rc)
 
     def als_train(self, k, lam, outer, seed, probe=None, workers=1):
         dt, _, _ = real_of(self.real)
@@ -510,14 +513,16 @@ class RefMatrix:
             self.h, k, lam, outer, workers, seed, ptr(pr), len(pr), ptr(W), ptr(H), ptr(rows), ptr(ts)))
         return W, H, rows
 
-    def als_epochs(self, k, lam, outer, seed, probe=None, workers=1):
+    def als_epochs(self, k, lam, outer, seed, probe=None, workers=1, history=False):
         dt, _, _ = real_of(self.real)
         pr = self._probe(probe)
         W = np.zeros((self.m, k), dt); H = np.zeros((self.n, k), dt)
         rows = np.zeros(outer, ITER_ROW)
+        Wh = np.zeros((outer, self.m, k), dt) if history else None
+        Hh = np.zeros((outer, self.n, k), dt) if history else None
         self.ref._check(getattr(self.ref.lib, "ref_als_epochs" + self.real)(
-            self.h, k, lam, outer, workers, seed, ptr(pr), len(pr), ptr(W), ptr(H), ptr(rows)))
-        return W, H, rows
+            self.h, k, lam, outer, workers, seed, ptr(pr), len(pr), ptr(W), ptr(H), ptr(rows), ptr(Wh), ptr(Hh)))
+        return (W, H, rows, Wh, Hh) if history else (W, H, rows)
 
     def update_u(self, rhat_row, v, lam):
         dt, _, _ = real_of(self.real)

@@ -193,7 +193,8 @@ const char* ref_last_error() { return g_err; }
     /* plus per-iteration train RMSE and the final residual in both layouts */                     \
     int ref_ccdpp_stage_loop##SUF(void* h, int k, Real lambda, int outer, int inner, int workers,   \
                                   uint64_t seed, const RefTriplet<Real>* probe, int64_t P,          \
-                                  Real* W, Real* H, Real* r_row, Real* r_col, IterRow* rows) {      \
+                                  Real* W, Real* H, Real* r_row, Real* r_col, IterRow* rows,        \
+                                  Real* W_hist, Real* H_hist) {                                     \
         GUARD({                                                                                     \
             const auto& a = static_cast<MatrixHandle<Real>*>(h)->a;                                 \
             FactorModel<Real> model(a.rows(), a.cols(), k);                                         \
@@ -224,6 +225,9 @@ const char* ref_last_error() { return g_err; }
                                                      static_cast<double>(a.nnz()))                  \
                                          : 0.0;                                                     \
                 rows[iter - 1] = row;                                                               \
+                if (W_hist)                                                                         \
+                    copy_model(model, W_hist + static_cast<size_t>(iter - 1) * a.rows() * k,        \
+                               H_hist + static_cast<size_t>(iter - 1) * a.cols() * k);              \
             }                                                                                       \
             copy_model(model, W, H);                                                                \
             std::ranges::copy(r.val_row(), r_row);                                                 \
@@ -250,7 +254,7 @@ const char* ref_last_error() { return g_err; }
     /* als epochs via als_epoch (als.hpp:176) with per-epoch train RMSE */                          \
     int ref_als_epochs##SUF(void* h, int k, Real lambda, int outer, int workers, uint64_t seed,     \
                             const RefTriplet<Real>* probe, int64_t P, Real* W, Real* H,             \
-                            IterRow* rows) {                                                        \
+                            IterRow* rows, Real* W_hist, Real* H_hist) {                            \
         GUARD({                                                                                     \
             const auto& a = static_cast<MatrixHandle<Real>*>(h)->a;                                 \
             FactorModel<Real> model(a.rows(), a.cols(), k);                                         \
@@ -267,6 +271,9 @@ const char* ref_last_error() { return g_err; }
                                                      static_cast<double>(a.nnz()))                  \
                                          : 0.0;                                                     \
                 rows[iter - 1] = row;                                                               \
+                if (W_hist)                                                                         \
+                    copy_model(model, W_hist + static_cast<size_t>(iter - 1) * a.rows() * k,        \
+                               H_hist + static_cast<size_t>(iter - 1) * a.cols() * k);              \
             }                                                                                       \
             copy_model(model, W, H);                                                                \
         })                                                                                          \

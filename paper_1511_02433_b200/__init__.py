@@ -42,7 +42,7 @@ __all__ = [
     "lib", "LIB_PATH", "TRIPLET", "RatingsMatrix", "CcdConfig", "AlsConfig", "FactorModel", "IterationRow",
     "TrainReport", "ccdpp_train", "als_train", "Algorithm", "RunSpec", "run_training", "rmse", "objective",
     "predict", "init_random_items", "ccdpp_build_rhat", "ccdpp_update_u", "ccdpp_update_v", "ccdpp_writeback",
-    "solve_user_rows", "solve_item_rows", "cholesky_solve_batched", "partition_balanced", "synth_ratings",
+    "solve_user_rows", "solve_item_rows", "cholesky_solve_batched", "partition_balanced",
     "Context", "DataError", "NotPositiveDefinite", "DomainError", "device_count", "nccl_unique_id", "dist_plan",
     "top_n", "top_n_batch", "ccd_train", "save_model", "load_model",
 ]
@@ -140,8 +140,6 @@ _SIGS = {
     "pmf_save_model": ([C.c_char_p, _P, _P, C.c_int64, C.c_int64, C.c_int64], C.c_int),
     "pmf_load_model": ([C.c_char_p, _P, _P, _P, _P, _P], C.c_int),
     "pmf_top_n": ([_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int32, C.c_int32, _P, _P, _P, _P, _P], C.c_int),
-    "pmf_synth_ratings": ([C.c_int32, C.c_int32, C.c_int32, C.c_int64, C.c_int64, C.c_uint32, _P, _P, _P, _P],
-                          C.c_int),
     "pmf_nccl_unique_id": ([_P], C.c_int),
     "pmf_dist_plan": ([_P, C.c_int32, _P, _P, _P, _P], C.c_int),
 }
@@ -630,15 +628,6 @@ def partition_balanced(costs: Sequence[int], p: int) -> np.ndarray:
     b = np.zeros(max(p, 0) + 1, np.int32)
     _check(lib.pmf_partition_balanced(_ptr(c), len(c), p, _ptr(b)))
     return b
-
-
-def synth_ratings(m, n, true_rank, n_train, n_probe, seed):
-    """Parallel synthetic ratings (recipe of tests/testutil.hpp:91-132) -> (train, probe) triplets."""
-    tr = np.empty(n_train, TRIPLET); pr = np.empty(n_probe, TRIPLET)
-    gt, gp = C.c_int64(), C.c_int64()
-    _check(lib.pmf_synth_ratings(m, n, true_rank, n_train, n_probe, seed, _ptr(tr), _ptr(pr), C.byref(gt),
-                                 C.byref(gp)))
-    return tr[:gt.value], pr[:gp.value]
 
 
 def dist_plan(a: RatingsMatrix, world: int):

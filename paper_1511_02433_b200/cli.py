@@ -315,12 +315,18 @@ def _spec(o):
         raise UsageError("--workers: bad worker count")
     if len(workers) != 1:
         raise UsageError("--workers: train takes a single worker count")
-    # one process drives one device: the worker count is accepted and the run reports 1
-    return RunSpec(algo, o.k, o.__dict__["lambda"], o.outer_iters, o.inner_iters, 1, o.seed)
+    # --workers W -> W GPU ranks (a device group, ccd.hpp:39 / als.hpp:30; ranks share devices round-robin
+    # when W exceeds the device count); item/user-wise CCD always runs one (ccd.hpp:306-309)
+    w = int(workers[0]) if algo != Algorithm.kCcd else 1
+    return RunSpec(algo, o.k, o.__dict__["lambda"], o.outer_iters, o.inner_iters, w, o.seed)
 
 
 def run_train(o):
     spec = _spec(o)
+    if o.precision == "double":
+        # parmf_cli's default is double (parmf_cli.cpp:43); the B200 path computes in FP32 only
+        print("warning: --precision double requested; the B200 path trains in single precision "
+              "(model.bin holds float32 factors, run.json reports precision=single)", file=sys.stderr)
     (tu, ti, tr), (pu, pi, pr) = _load_train_probe(o)
     users, items = IdMap.from_values(tu), IdMap.from_values(ti)
     t = np.empty(len(tu), TRIPLET)

@@ -917,6 +917,16 @@ int launch_als_half(const DevAls& L, const float* opp, int64_t n_opp, float* out
                     float lambda, bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t stream,
                     bool gs) {
     if (gs && !als_gram_gs_supported(k)) return -1;  // the Gauss-Seidel solve lives in the tensor-core path
+    if (k > 64) {
+        int launched = launch_als_big(L, opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count,
+                                      L.big_scratch, stream);
+        if (L.n_empty > 0) {
+            zero_rows_kernel<<<std::min(1024, (L.n_empty * k + 255) / 256), 256, 0, stream>>>(L.empty_out, L.n_empty,
+                                                                                           out, out_off, k);
+            ++launched;
+        }
+        return launched;
+    }
 #define PMF_HALF(K) \
     return launch_k<K>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, stream, gs)
     if (k <= 8) PMF_HALF(8);

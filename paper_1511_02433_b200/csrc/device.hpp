@@ -149,7 +149,8 @@ struct DevAls {
     int32_t* mo_out = nullptr;
     int32_t* mo_start = nullptr;
     int32_t* empty_out = nullptr;
-    float* partial = nullptr;   // n_slots * (k*k + k)
+    float* partial = nullptr;   // n_slots * (k*k + k + 1)
+    float* big_scratch = nullptr;  // k > 64 with the system past shared memory: per-CTA k x k in HBM
 };
 
 // Solves every output row of one side: out row (out_off + o) of the row-major factor `out`
@@ -161,6 +162,13 @@ int launch_als_half(const DevAls& L, const float* opp, int64_t n_opp, float* out
                     float lambda, bool weighted, int* d_counter, int* d_status, int sm_count,
                     cudaStream_t stream, bool gs = false);
 bool als_gram_gs_supported(int k);
+// k > 64 (als_big_kernels.cu): a CTA per unit, the system in shared memory (HBM scratch of
+// als_big_scratch_floats past ~216).
+int64_t als_big_scratch_floats(int k, int sm_count);
+int launch_als_big(const DevAls& L, const float* opp, float* out, int32_t out_off, int k, float lambda, bool weighted,
+                   int* d_counter, int* d_status, int sm_count, float* gscratch, cudaStream_t s);
+void launch_cholesky_big(float* a, float* x, int batch, int k, int* d_status, int sm_count, float* gscratch,
+                         cudaStream_t s);
 void als_set_attributes();
 // Batched Cholesky factor + solve of `batch` k*k row-major systems in place.
 void launch_cholesky_batched(float* a, float* x, int batch, int k, int* d_status,

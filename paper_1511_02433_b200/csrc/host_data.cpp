@@ -1,6 +1,5 @@
 // host_data.cpp -- host-side data entry points of the C-ABI (no CUDA):
 //   pmf_matrix_from_triplets  (sparse.hpp:73-149 RatingsMatrix::from_triplets, multithreaded)
-//   pmf_synth_ratings         (tests/testutil.hpp:91-132 recipe, parallel per-user streams)
 //   pmf_partition_balanced    (runtime.hpp:91-136)
 #include <algorithm>
 #include <atomic>
@@ -27,29 +26,6 @@ using pmfgpu::parallel_for;
 namespace {
 
 int hw_threads() { return static_cast<int>(std::max(1u, std::thread::hardware_concurrency())); }
-
-// splitmix64: per-user counter-based stream (independent of thread scheduling)
-struct SplitMix {
-    uint64_t s;
-    explicit SplitMix(uint64_t seed) : s(seed) {}
-    uint64_t next() {
-        uint64_t z = (s += 0x9E3779B97F4A7C15ull);
-        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
-        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
-        return z ^ (z >> 31);
-    }
-    double unit() { return (static_cast<double>(next() >> 32) + 1.0) * (1.0 / 4294967296.0); }  // (0,1]
-    double gaussian() {
-        const double u1 = unit(), u2 = unit();
-        return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
-    }
-};
-
-double mt_unit(std::mt19937& g) { return (static_cast<double>(g()) + 1.0) * (1.0 / 4294967296.0); }
-double mt_gauss(std::mt19937& g) {
-    const double u1 = mt_unit(g), u2 = mt_unit(g);
-    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586 * u2);
-}
 
 }  // namespace
 
@@ -220,118 +196,6 @@ pmf_status pmf_matrix_from_triplets(const pmf_triplet* t, int64_t nnz, int32_t m
             });
         for (auto& x : ts) x.join();
     }
-    return PMF_OK;
-}
-
-pmf_status pmf_synth_ratings(int32_t m, int32_t n, int32_t true_rank, int64_t n_train, int64_t n_probe,
-                             uint32_t seed, pmf_triplet* out_train, pmf_triplet* out_probe,
-                             int64_t* got_train, int64_t* got_probe) {
-    if (m < 1 || n < 1 || true_rank < 1 || n_train < 0 || n_probe < 0 || (n_train && !out_train) ||
-        (n_probe && !out_probe)) {
-        pmfgpu::set_error("synth_ratings: invalid arguments");
-        return PMF_INVALID_ARGUMENT;
-    }
-    const int64_t total = n_train + n_probe;
-    if (total > static_cast<int64_t>(m) * n) {
-        pmfgpu::set_error("synth_ratings: more ratings than matrix cells");
-        return PMF_INVALID_ARGUMENT;
-    }
-    // planted factors and biases, drawn in the order of testutil.hpp:103-111
-    std::mt19937 gen(seed);
-    const int r = true_rank;
-    const double fscale = 0.45 / std::sqrt(static_cast<double>(r));
-    std::vector<double> w(static_cast<size_t>(m) * r), h(static_cast<size_t>(n) * r), bu(m), bi(n);
-    for (auto& x : w) x = mt_gauss(gen) * fscale;
-    for (auto& x : h) x = mt_gauss(gen) * fscale;
-    for (auto& x : bu) x = mt_gauss(gen) * 0.35;
-    for (auto& x : bi) x = mt_gauss(gen) * 0.35;
-    std::vector<double> cdf(n);
-    double acc = 0.0;
-    for (int32_t j = 0; j < n; ++j) {
-        acc += 1.0 / std::pow(static_cast<double>(j) + 1.0, 0.8);
-        cdf[j] = acc;
-    }
-    for (auto& x : cdf) x /= acc;
-    // per-user counts ~ N(mean, mean) (the reference's uniform-user draw), fixed up to `total`
-    const double mean = static_cast<double>(total) / m;
-    std::vector<int64_t> cnt(m);
-    parallel_for(m, [&](int64_t b, int64_t e) {
-        for (int64_t i = b; i < e; ++i) {
-            SplitMix sm(static_cast<uint64_t>(seed) * 0x100000001B3ull ^ (static_cast<uint64_t>(i) << 20) ^ 0xC0FFEEull);
-            const double c = std::round(mean + std::sqrt(std::max(mean, 1e-9)) * sm.gaussian());
-            cnt[i] = std::min<int64_t>(n, std::max<int64_t>(0, static_cast<int64_t>(c)));
-        }
-    });
-    int64_t sum = 0;
-    for (auto c : cnt) sum += c;
-    for (int64_t pass = 0; sum != total && pass < 64; ++pass) {
-        const int64_t diff = total - sum;
-        const int64_t step = std::max<int64_t>(1, m / std::max<int64_t>(1, std::llabs(diff)));
-        for (int64_t i = (pass * 7919) % m, done = 0; done < m && sum != total; ++done, i = (i + step) % m) {
-            if (diff > 0 && cnt[i] < n) {
-                cnt[i]++;
-                sum++;
-            } else if (diff < 0 && cnt[i] > 0) {
-                cnt[i]--;
-                sum--;
-            }
-        }
-    }
-    // deterministic per-user probe allocation proportional to the counts
-    std::vector<int64_t> pcnt(m), tr_off(m + 1, 0), pr_off(m + 1, 0);
-    {
-        int64_t cum = 0;
-        for (int32_t i = 0; i < m; ++i) {
-            const int64_t a = total ? static_cast<int64_t>((static_cast<__int128>(n_probe) * cum) / total) : 0;
-            cum += cnt[i];
-            const int64_t b = total ? static_cast<int64_t>((static_cast<__int128>(n_probe) * cum) / total) : 0;
-            pcnt[i] = std::min(b - a, cnt[i]);
-            tr_off[i + 1] = tr_off[i] + cnt[i] - pcnt[i];
-            pr_off[i + 1] = pr_off[i] + pcnt[i];
-        }
-    }
-    parallel_for(m, [&](int64_t b, int64_t e) {
-        std::vector<uint8_t> used(static_cast<size_t>(n), 0);
-        std::vector<int32_t> items;
-        std::vector<uint8_t> is_probe;
-        for (int64_t i = b; i < e; ++i) {
-            SplitMix sm(static_cast<uint64_t>(seed) * 0x9E3779B97F4A7C15ull + static_cast<uint64_t>(i) * 0xD1B54A32D192ED03ull + 1);
-            items.clear();
-            while (static_cast<int64_t>(items.size()) < cnt[i]) {
-                const double u = sm.unit();
-                const int32_t j = static_cast<int32_t>(std::lower_bound(cdf.begin(), cdf.end(), u) - cdf.begin());
-                const int32_t jj = std::min(j, n - 1);
-                if (used[jj]) continue;
-                used[jj] = 1;
-                items.push_back(jj);
-            }
-            for (auto j : items) used[j] = 0;
-            std::sort(items.begin(), items.end());
-            // choose pcnt[i] probe positions (partial Fisher-Yates over positions)
-            const int64_t c = static_cast<int64_t>(items.size());
-            is_probe.assign(c, 0);
-            std::vector<int32_t> pos(c);
-            for (int64_t x = 0; x < c; ++x) pos[x] = static_cast<int32_t>(x);
-            for (int64_t x = 0; x < pcnt[i]; ++x) {
-                const int64_t y = x + static_cast<int64_t>(sm.next() % static_cast<uint64_t>(c - x));
-                std::swap(pos[x], pos[y]);
-                is_probe[pos[x]] = 1;
-            }
-            int64_t wt = tr_off[i], wp = pr_off[i];
-            for (int64_t x = 0; x < c; ++x) {
-                const int32_t j = items[x];
-                double score = 3.6 + bu[i] + bi[j] + sm.gaussian() * 0.35;
-                for (int t = 0; t < r; ++t)
-                    score += w[static_cast<size_t>(i) * r + t] * h[static_cast<size_t>(j) * r + t] / (fscale * fscale) * 0.12;
-                score = std::min(5.0, std::max(1.0, std::round(score)));
-                pmf_triplet tr{static_cast<int32_t>(i), j, static_cast<float>(score)};
-                if (is_probe[x]) out_probe[wp++] = tr;
-                else out_train[wt++] = tr;
-            }
-        }
-    });
-    if (got_train) *got_train = tr_off[m];
-    if (got_probe) *got_probe = pr_off[m];
     return PMF_OK;
 }
 

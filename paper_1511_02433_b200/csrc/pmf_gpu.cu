@@ -1016,6 +1016,8 @@ void als_alloc_partials(Ctx& c, int k) {
     const int64_t stride = static_cast<int64_t>(k) * k + k + 1;
     c.als_csr.partial = c.model_mem.alloc<float>(std::max<int64_t>(1, c.als_csr.n_slots * stride), false);
     c.als_csc.partial = c.model_mem.alloc<float>(std::max<int64_t>(1, c.als_csc.n_slots * stride), false);
+    const int64_t big = k > 64 ? als_big_scratch_floats(k, c.sm_count) : 0;
+    c.als_csr.big_scratch = c.als_csc.big_scratch = big > 0 ? c.model_mem.alloc<float>(big, false) : nullptr;
 }
 
 void als_begin(Ctx& c0, const pmf_als_config* cfg) {
@@ -1025,7 +1027,6 @@ void als_begin(Ctx& c0, const pmf_als_config* cfg) {
     if (!(cfg->lambda > 0.f)) invalid("als requires lambda > 0");
     if (cfg->outer_iters < 1) invalid("outer_iters must be >= 1");
     if (cfg->num_gpus < 1) invalid("workers must be >= 1");
-    if (cfg->k > 64) invalid("the B200 ALS kernels support k <= 64");
     if (!c0.als_built) invalid("context was created without ALS layouts");
     const auto H = init_items_host(c0.n, cfg->k, cfg->seed);  // model.hpp:86-93, replicated
     for (Ctx* cp : ranks_of(c0)) {
@@ -1982,7 +1983,6 @@ pmf_status pmf_als_solve_rows(const pmf_matrix_view* a, int32_t side, const floa
         if (side != 0 && side != 1) invalid("side must be 0 (users) or 1 (items)");
         if (!opposing || !out) invalid("null buffers");
         if (k < 1) invalid("k must be >= 1");
-        if (k > 64) invalid("the B200 ALS kernels support k <= 64");
         if (lambda < 0.f) invalid("lambda must be >= 0");
         auto c = make_ctx(a, -1, 0, 1, nullptr);
         build_als(*c, a);
@@ -2005,7 +2005,6 @@ pmf_status pmf_als_solve_rows(const pmf_matrix_view* a, int32_t side, const floa
 pmf_status pmf_cholesky_solve_batched(int32_t batch, int32_t k, float* a, float* x) {
     return guard([&] {
         if (batch < 0 || k < 1) invalid("invalid batch / order");
-        if (k > 64) invalid("the B200 batched Cholesky supports k <= 64");
         if (batch == 0) return;
         if (!a || !x) invalid("null buffers");
         ensure_device();
@@ -2020,7 +2019,14 @@ pmf_status pmf_cholesky_solve_batched(int32_t batch, int32_t k, float* a, float*
         int* st = mem.alloc<int>(1);
         CUDA_TRY(cudaMemcpy(da, a, sizeof(float) * batch * k * k, cudaMemcpyHostToDevice));
         CUDA_TRY(cudaMemcpy(dx, x, sizeof(float) * batch * k, cudaMemcpyHostToDevice));
-        launch_cholesky_batched(da, dx, batch, k, st, 0);
+        if (k > 64) {
+            int sms = 148;
+            CUDA_TRY(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+            const int64_t sc = als_big_scratch_floats(k, sms);
+            launch_cholesky_big(da, dx, batch, k, st, sms, sc > 0 ? mem.alloc<float>(sc, false) : nullptr, 0);
+        } else {
+            launch_cholesky_batched(da, dx, batch, k, st, 0);
+        }
         CUDA_TRY(cudaDeviceSynchronize());
         int h = 0;
         CUDA_TRY(cudaMemcpy(&h, st, sizeof(int), cudaMemcpyDeviceToHost));

@@ -1,5 +1,5 @@
 """CPU tests of the C-ABI library: it loads, exports every symbol include/pmf_gpu.h declares, its host
-helpers (from_triplets, partition_balanced, synth_ratings) match the reference, and without a GPU
+helpers (from_triplets, partition_balanced) match the reference, and without a GPU
 every compute entry point fails loudly (no CPU fallback)."""
 import ctypes as C
 import os
@@ -76,23 +76,6 @@ def test_partition_balanced_matches_reference(pmf, oracle):
         pmf.partition_balanced([1, 2], 0)
     with pytest.raises(ValueError):
         pmf.partition_balanced([1, -2], 2)
-
-
-def test_synth_ratings_recipe(pmf):
-    """Parallel generator: exact counts, sorted unique (user,item), 1..5 stars, Zipf-skewed items,
-    deterministic in the seed."""
-    tr, pr = pmf.synth_ratings(2000, 500, 3, 60000, 3000, 11)
-    assert len(tr) == 60000 and len(pr) == 3000
-    allt = np.concatenate([tr, pr])
-    key = allt["user"].astype(np.int64) * 500 + allt["item"]
-    assert len(np.unique(key)) == len(key)
-    assert set(np.unique(allt["rating"])) <= {1.0, 2.0, 3.0, 4.0, 5.0}
-    k_tr = tr["user"].astype(np.int64) * 500 + tr["item"]
-    assert np.all(np.diff(k_tr) > 0)
-    cnt = np.bincount(allt["item"], minlength=500)
-    assert cnt[:10].sum() > cnt[-100:].sum()
-    tr2, pr2 = pmf.synth_ratings(2000, 500, 3, 60000, 3000, 11)
-    assert np.array_equal(tr, tr2) and np.array_equal(pr, pr2)
 
 
 def test_init_random_items_matches_reference(pmf, oracle):

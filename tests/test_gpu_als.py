@@ -43,19 +43,42 @@ def test_solve_rows_normal_equations(pmf, oracle):
                 assert np.max(np.abs(r)) < 2e-4 * max(1.0, np.max(np.abs(Hs.T @ a)))
 
 
-@pytest.mark.parametrize("k", [1, 3, 8, 10, 16, 20, 32, 40, 50, 64])
+@pytest.mark.parametrize("k", [1, 3, 8, 10, 16, 20, 32, 40, 50, 64, 65, 100, 128, 240])
 def test_solve_rows_vs_oracle(pmf, oracle, k):
+    """One W half-step and one H half-step against the oracle (= the reference's solve_row, pinned in
+    test_oracle.py).  Tolerance: 1e-3 relative Frobenius, or twice the reference's own float-vs-double
+    distance on the same inputs where that is larger (30 ratings per row against k up to 240 leaves
+    the systems ill-conditioned: lambda = 0.05 is all that keeps them positive definite).  k > 64 runs
+    the CTA-per-unit kernels (shared-memory system; HBM scratch at k = 240)."""
     t = oracle.synth_ratings(200, 120, 3, 6000, 7)
     A = pmf.RatingsMatrix.from_triplets(t, 200, 120)
     O = oracle.from_triplets(t, 200, 120)
+    O64 = oracle.from_triplets(t, 200, 120, "_f64")
     rng = np.random.default_rng(k)
     h = (rng.uniform(0, 1, (120, k)) / math.sqrt(k)).astype(np.float32)
     w_gpu = pmf.solve_user_rows(A, h, k, 0.05)
     w_ref = oracle.als_half(O, 0, h, 0.05)
-    assert frob_rel(w_gpu, w_ref) < 2e-3
+    w_64 = oracle.als_half(O64, 0, h.astype(np.float64), 0.05, "_f64")
+    assert frob_rel(w_gpu, w_ref) <= max(1e-3, 2 * frob_rel(w_ref, w_64))
     hh = pmf.solve_item_rows(A, w_ref, k, 0.05)
     h_ref = oracle.als_half(O, 1, w_ref, 0.05)
-    assert frob_rel(hh, h_ref) < 2e-3
+    h_64 = oracle.als_half(O64, 1, w_ref.astype(np.float64), 0.05, "_f64")
+    assert frob_rel(hh, h_ref) <= max(1e-3, 2 * frob_rel(h_ref, h_64))
+
+
+@pytest.mark.parametrize("k", [65, 100])
+def test_als_large_k_trajectory(pmf, oracle, ml100k, k):
+    """als_train past k = 64 (the reference has no bound, als.hpp:26-40): per-iteration metrics within
+    1e-4 of the oracle, factors within 1e-3."""
+    train, probe = ml100k
+    A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
+    model, rep = pmf.als_train(pmf.AlsConfig(k=k, lam=0.05, outer_iters=3, seed=1), A, probe)
+    O = oracle.from_triplets(train, 943, 1682)
+    W, H, rows = oracle.als_train(O, k, 0.05, 3, 1, probe)
+    for r, g in zip(rep.rows, rows):
+        for f in ("objective", "rmse", "train_rmse"):
+            assert rel(getattr(r, f), float(g[f])) < 1e-4, (f, r, g[f])
+    assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
 
 
 def test_long_columns_use_chunked_partials(pmf, oracle):
@@ -125,7 +148,7 @@ def test_cholesky_batched_known_answers(pmf, oracle):
     with pytest.raises(ArithmeticError):
         pmf.cholesky_solve_batched(np.array([[1.0, 2.0], [2.0, 1.0]]), np.array([1.0, 1.0]))
     rng = np.random.default_rng(606)   # acceptance C10 in FP32: reconstruction and solve residual
-    for k in (1, 2, 5, 10, 40):
+    for k in (1, 2, 5, 10, 40, 64, 65, 100, 240):
         b = rng.uniform(-1, 1, (16, k, k))
         spd = b @ np.transpose(b, (0, 2, 1)) + 0.1 * np.eye(k)
         rhs = rng.uniform(-5, 5, (16, k))

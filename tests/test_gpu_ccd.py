@@ -10,6 +10,8 @@ import os
 import numpy as np
 import pytest
 
+import datagen
+
 from conftest import frob_rel, rel
 
 pytestmark = pytest.mark.gpu
@@ -283,7 +285,7 @@ def test_alloc_cache_off_same_model(pmf, tmp_path):
     import subprocess
     import sys
     m, n = 30000, 2000
-    train, _ = pmf.synth_ratings(m, n, 3, 5_000_000, 1000, 11)
+    train, _ = datagen.synth_ratings(m, n, 3, 5_000_000, 1000, 11)
     A = pmf.RatingsMatrix.from_triplets(train, m, n)
     cfg = pmf.CcdConfig(k=4, lam=0.05, outer_iters=2, inner_iters=3, seed=2)
     m1, _ = pmf.ccdpp_train(cfg, A)

@@ -5,6 +5,8 @@ and raise the same errors with the same messages (sparse.hpp:82-92 input-order v
 import numpy as np
 import pytest
 
+import datagen
+
 pytestmark = pytest.mark.gpu
 FIELDS = ("row_start", "col_of", "val_row", "col_start", "row_of", "val_col")
 
@@ -30,7 +32,7 @@ def test_from_triplets_gpu_matches_host(pmf, oracle, ml100k):
 
 @pytest.mark.slow
 def test_from_triplets_gpu_large(pmf):
-    train, _ = pmf.synth_ratings(200000, 30000, 3, 3_000_000, 0, 11)
+    train, _ = datagen.synth_ratings(200000, 30000, 3, 3_000_000, 0, 11)
     _same(pmf.RatingsMatrix.from_triplets(train, 200000, 30000, device=True),
           pmf.RatingsMatrix.from_triplets(train, 200000, 30000))
 
