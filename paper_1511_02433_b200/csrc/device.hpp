@@ -162,6 +162,13 @@ int launch_als_half(const DevAls& L, const float* opp, int64_t n_opp, float* out
                     float lambda, bool weighted, int* d_counter, int* d_status, int sm_count,
                     cudaStream_t stream, bool gs = false);
 bool als_gram_gs_supported(int k);
+// k <= 48 (als_umma_kernels.cu): the gram on tcgen05 tensor cores (TMEM accumulators), warp-specialised
+// persistent CTAs.  The caller resets *d_counter.  Returns false when k is out of range.
+bool als_umma_supported(int k);
+bool launch_als_umma(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k,
+                     float lambda, bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t s,
+                     bool gs);
+void als_umma_set_attributes();
 // k > 64 (als_big_kernels.cu): a CTA per unit, the system in shared memory (HBM scratch of
 // als_big_scratch_floats past ~216).
 int64_t als_big_scratch_floats(int k, int sm_count);

@@ -69,16 +69,22 @@ def test_solve_rows_vs_oracle(pmf, oracle, k):
 @pytest.mark.parametrize("k", [65, 100])
 def test_als_large_k_trajectory(pmf, oracle, ml100k, k):
     """als_train past k = 64 (the reference has no bound, als.hpp:26-40): per-iteration metrics within
-    1e-4 of the oracle, factors within 1e-3."""
+    1e-4 of the oracle; factors within 1e-3, or within twice the reference's own float-vs-double
+    factor distance at this k, computed here (the oracle is bitwise the reference in both precisions):
+    at k = 100 the float and double runs are 1.8e-3 (W) / 3.6e-3 (H) apart after 3 iterations, so
+    FP32 reduction order alone moves the factors past 1e-3."""
     train, probe = ml100k
     A = pmf.RatingsMatrix.from_triplets(train, 943, 1682)
     model, rep = pmf.als_train(pmf.AlsConfig(k=k, lam=0.05, outer_iters=3, seed=1), A, probe)
     O = oracle.from_triplets(train, 943, 1682)
     W, H, rows = oracle.als_train(O, k, 0.05, 3, 1, probe)
+    O64 = oracle.from_triplets(train, 943, 1682, "_f64")
+    W64, H64, _ = oracle.als_train(O64, k, 0.05, 3, 1, probe, real="_f64")
     for r, g in zip(rep.rows, rows):
         for f in ("objective", "rmse", "train_rmse"):
             assert rel(getattr(r, f), float(g[f])) < 1e-4, (f, r, g[f])
-    assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+    assert frob_rel(model.w, W) <= max(1e-3, 2 * frob_rel(W, W64))
+    assert frob_rel(model.h, H) <= max(1e-3, 2 * frob_rel(H, H64))
 
 
 def test_long_columns_use_chunked_partials(pmf, oracle):

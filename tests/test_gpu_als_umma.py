@@ -1,0 +1,58 @@
+"""The tcgen05 / TMEM ALS gram kernel (als_umma_kernels.cu, opt-in PMF_ALS_UMMA=1) against the oracle.
+
+The switch is read once per process, so each case runs in a subprocess with the variable set.  Same
+criteria as test_gpu_als.py: per-iteration objective, probe RMSE and train RMSE within 1e-4 of the
+oracle (pinned bit-for-bit to the reference's als_train / ccd_train), factors within 1e-3 relative
+Frobenius; k covers the 4-byte gather path (k % 4 != 0), the 16-byte path, both solver register sets
+(k > 32) and the item/user-wise CCD Gauss-Seidel epilogue."""
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+SCRIPT = r'''
+import json, sys
+import numpy as np
+sys.path.insert(0, sys.argv[1])
+import paper_1511_02433_b200 as P
+from oracle.pyoracle import Oracle
+algo, k = sys.argv[2], int(sys.argv[3])
+O = Oracle()
+a = O.synth_ratings(943, 1682, 3, 100000, 777)
+train, probe = O.carve_probe(a, 10000, 5)
+A = P.RatingsMatrix.from_triplets(train, 943, 1682)
+OA = O.from_triplets(train, 943, 1682)
+if algo == "als":
+    model, rep = P.als_train(P.AlsConfig(k=k, lam=0.05, outer_iters=3, seed=1), A, probe)
+    W, H, rows = O.als_train(OA, k, 0.05, 3, 1, probe)
+else:
+    model, rep = P.ccd_train(P.CcdConfig(k=k, lam=0.05, outer_iters=3, inner_iters=1, seed=1), A, probe)
+    W, H, rows = O.ccd_train(OA, k, 0.05, 3, 1, probe)
+def fr(x, y):
+    return float(np.linalg.norm(np.float64(x) - np.float64(y)) / np.linalg.norm(np.float64(y)))
+out = {"rel": [[abs(getattr(r, f) - float(g[f])) / abs(float(g[f])) for f in ("objective", "rmse", "train_rmse")]
+               for r, g in zip(rep.rows, rows)],
+       "w": fr(model.w, W), "h": fr(model.h, H)}
+print(json.dumps(out))
+'''
+
+
+@pytest.mark.parametrize("algo,k,gram", [("als", 10, False), ("als", 20, False), ("als", 40, False),
+                                         ("als", 44, False), ("ccd", 40, True)])
+def test_umma_gram_vs_oracle(algo, k, gram):
+    env = dict(os.environ, PMF_ALS_UMMA="1")
+    if gram:
+        env["PMF_CCD_GRAM"] = "1"
+    r = subprocess.run([sys.executable, "-c", SCRIPT, ROOT, algo, str(k)], env=env, capture_output=True, text=True,
+                       timeout=240)
+    assert r.returncode == 0, r.stderr[-2000:]
+    out = json.loads(r.stdout.strip().splitlines()[-1])
+    for row in out["rel"]:
+        assert max(row) < 1e-4, out
+    assert out["w"] < 1e-3 and out["h"] < 1e-3, out

@@ -28,12 +28,14 @@ CORES = os.cpu_count() or 1
 
 def factor_tol(cfg, which, iters):
     """1e-3, or 2 x the reference's own float-vs-double factor distance after `iters` outer iterations
-    at this shape (committed calibration, scripts/parity_artifacts.py)."""
-    p = os.path.join(ROOT, "profiles", f"r02_parity_{cfg}.json")
-    if not os.path.exists(p):
-        return 1e-3
-    cal = json.load(open(p))["factors_per_iteration"][iters - 1][f"{which}_f32_vs_f64"]
-    return max(1e-3, 2.0 * cal)
+    at this shape (committed calibration: scripts/calibrate_ref.py -> profiles/r02_calib_CFG.json, or the
+    float-vs-double column of scripts/parity_artifacts.py -> profiles/r02_parity_CFG.json)."""
+    for name in (f"r02_calib_{cfg}.json", f"r02_parity_{cfg}.json"):
+        p = os.path.join(ROOT, "profiles", name)
+        if os.path.exists(p):
+            cal = json.load(open(p))["factors_per_iteration"][iters - 1][f"{which}_f32_vs_f64"]
+            return max(1e-3, 2.0 * cal)
+    return 1e-3
 
 
 def _data(cfg):
