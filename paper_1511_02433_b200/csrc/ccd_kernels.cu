@@ -29,7 +29,14 @@ namespace {
 
 constexpr int kDefaultPlainVariantCsr = 1;  // u-sweep: 1024 threads, unroll 4/2/2
 constexpr int kDefaultPlainVariantCsc = 2;  // v-sweep: 1024 threads, unroll 2/2/2
-constexpr int kDefaultPromoteVariant = 0;
+#ifndef PMF_PROMOTE_VARIANT_CSR
+#define PMF_PROMOTE_VARIANT_CSR 0
+#endif
+#ifndef PMF_PROMOTE_VARIANT_CSC
+#define PMF_PROMOTE_VARIANT_CSC 0
+#endif
+constexpr int kDefaultPromoteVariantCsr = PMF_PROMOTE_VARIANT_CSR;  // 512 threads, unroll 8/4/4
+constexpr int kDefaultPromoteVariantCsc = PMF_PROMOTE_VARIANT_CSC;
 
 // Launch variants (threads per CTA, unroll of the long / medium / short length classes).  More
 // resident warps keep more loads in flight (scripts/micro/stream_bw.cu: 8 warps/SM cap at ~4 TB/s,
@@ -117,8 +124,11 @@ struct IdxVec<false> {
 template <int MODE, bool CSR>
 struct Roles {
     // staged arrays: plain: s0 = gn;  promote CSR: s0 = ga, s1 = gb (gn == gb);
-    // promote CSC: s0 = ga, s1 = gb, s2 = gn;  demote: s0 = ga.
-    static constexpr int kArrays = MODE == kPromote ? (CSR ? 2 : 3) : MODE == kRmw ? 2 : 1;
+    // promote CSC: s0 = gb, s1 = gn, and the demote's ga read through L1 (kGaL1): three staged vectors
+    // (225 KB at Netflix panel widths) leave ~28 KB of L1 and put the sweep on the L1 cliff
+    // (DESIGN.md 4); with two, the ~75 KB ga slice of a panel stays L1-resident;  demote: s0 = ga.
+    static constexpr bool kGaL1 = MODE == kPromote && !CSR;
+    static constexpr int kArrays = MODE == kPromote ? 2 : MODE == kRmw ? 2 : 1;
 };
 
 __host__ __device__ __forceinline__ int stage_stride(int panel_size) { return ((panel_size + 1) + 3) & ~3; }
@@ -129,7 +139,7 @@ constexpr int kStealRestageMin = 16384;
 
 // Processes units [ub, ue) of the current piece in warp batches of 32/G units, one unit per group
 // of G lanes.  `counter` is the piece's shared counter for this length class.
-template <int MODE, bool CSR, bool IDX16, int G, int kUnroll>
+template <int MODE, bool CSR, bool IDX16, int G, int kUnroll, bool GA_GLOBAL = false>
 __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, const Unit* __restrict__ units,
                                           const void* __restrict__ idx, float* __restrict__ R,
                                           float2* __restrict__ partial, const SweepOperands& op,
@@ -203,7 +213,10 @@ __device__ __noinline__ void run_class(int* counter, int32_t ub, int32_t ue, con
                             const float h = CSR ? b : ob;
                             if (w != 0.f) r = __fadd_rn(r, __fmul_rn(w, h));
                         } else {
-                            const float a = g0[gi];
+                            // CSC: g0 is global memory (the panel's ga slice, read through L1) and the
+                            // padding entries' sentinel index must read 0 as the staged sentinel slot does
+                            const float a = Roles<MODE, CSR>::kGaL1 && GA_GLOBAL ? (gi < op.psz ? __ldg(g0 + gi) : 0.f)
+                                                                                  : g0[gi];
                             const float b = g1[gi];
                             // deferred writeback of the previous step: R - u'_i v'_j
                             r = __fsub_rn(r, __fmul_rn(oa, a));
@@ -409,9 +422,14 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
                     const uint32_t bytes = static_cast<uint32_t>(((len + 3) & ~3) * sizeof(float));
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     mbar_expect_tx(&s_bar, bytes * A);
-                    bulk_g2s(s0, (MODE == kPlain ? op.gn : op.ga) + gbase, bytes, &s_bar);
-                    if (A >= 2) bulk_g2s(s1, op.gb + gbase, bytes, &s_bar);
-                    if (A >= 3) bulk_g2s(s2, op.gn + gbase, bytes, &s_bar);
+                    if (Roles<MODE, CSR>::kGaL1) {
+                        bulk_g2s(s0, op.gb + gbase, bytes, &s_bar);
+                        bulk_g2s(s1, op.gn + gbase, bytes, &s_bar);
+                    } else {
+                        bulk_g2s(s0, (MODE == kPlain ? op.gn : op.ga) + gbase, bytes, &s_bar);
+                        if (A >= 2) bulk_g2s(s1, op.gb + gbase, bytes, &s_bar);
+                        if (A >= 3) bulk_g2s(s2, op.gn + gbase, bytes, &s_bar);
+                    }
                 }
             }
             if (SMEM && stage) {
@@ -428,6 +446,11 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
             const float* g0 = SMEM ? s0 : (MODE == kPlain ? op.gn : op.ga);
             const float* g1 = SMEM ? s1 : op.gb;
             const float* g2 = SMEM ? s2 : op.gn;
+            if (Roles<MODE, CSR>::kGaL1 && SMEM) {
+                g0 = op.ga + panel_base[pz.panel];
+                g1 = s0;
+                g2 = s1;
+            }
             if constexpr (MODE == kRmw && SMEM) {
                 if (nsub > 1) {
                     const int32_t gofs = q * panel_size;
@@ -437,9 +460,10 @@ sweep_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces,
                     continue;
                 }
             }
-            run_class<MODE, CSR, IDX16, 8, Var<V>::UA>(c0, pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
-            run_class<MODE, CSR, IDX16, 4, Var<V>::UB>(c1, pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
-            run_class<MODE, CSR, IDX16, 2, Var<V>::UC>(c2, pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
+            constexpr bool kGG = Roles<MODE, CSR>::kGaL1 && SMEM;
+            run_class<MODE, CSR, IDX16, 8, Var<V>::UA, kGG>(c0, pz.ub, pz.um, units, idx, R, partial, op, g0, g1, g2);
+            run_class<MODE, CSR, IDX16, 4, Var<V>::UB, kGG>(c1, pz.um, pz.us, units, idx, R, partial, op, g0, g1, g2);
+            run_class<MODE, CSR, IDX16, 2, Var<V>::UC, kGG>(c2, pz.us, pz.ue, units, idx, R, partial, op, g0, g1, g2);
         }
     }
     if (steal) {
@@ -561,8 +585,10 @@ bool steal_enabled(const DevSweep& L) {
 template <int MODE, bool CSR, bool IDX16, bool SMEM, int V>
 void launch_one(const DevSweep& L, const SweepOperands& op, size_t smem, cudaStream_t s) {
     const bool sub = MODE == kRmw && L.rmw_sub > 1;
+    SweepOperands o = op;
+    o.psz = sub ? L.sub_width : L.panel_size;
     sweep_kernel<MODE, CSR, IDX16, SMEM, V><<<L.ctas, Var<V>::NT, smem, s>>>(
-        L.units, L.pieces, L.piece_start, L.panel_base, L.idx, L.R, L.partial, op,
+        L.units, L.pieces, L.piece_start, L.panel_base, L.idx, L.R, L.partial, o,
         sub ? L.sub_width : L.panel_size, L.usplit, sub ? L.rmw_sub : 1, steal_enabled(L) ? L.gcnt : nullptr,
         L.n_pieces);
 }
@@ -572,7 +598,7 @@ void launch_one(const DevSweep& L, const SweepOperands& op, size_t smem, cudaStr
 int variant_for(int mode, bool csr) {
     if (mode == kRmw) return 2;
     if (mode == kPlain) return csr ? kDefaultPlainVariantCsr : kDefaultPlainVariantCsc;
-    return kDefaultPromoteVariant;
+    return csr ? kDefaultPromoteVariantCsr : kDefaultPromoteVariantCsc;
 }
 
 template <int MODE, bool CSR>
@@ -611,7 +637,7 @@ void set_attr_all(size_t max_smem) {
 
 size_t sweep_smem_bytes(const DevSweep& L, SweepMode mode, bool csr_side) {
     if (!L.smem) return 0;
-    const int arrays = mode == kPromote ? (csr_side ? 2 : 3) : mode == kRmw ? 2 : 1;
+    const int arrays = mode == kPromote ? 2 : mode == kRmw ? 2 : 1;  // CSC promote: ga through L1
     const int width = mode == kRmw && L.rmw_sub > 1 ? L.sub_width : L.panel_size;
     return static_cast<size_t>(arrays) * stage_stride(width) * sizeof(float);
 }

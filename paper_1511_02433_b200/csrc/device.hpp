@@ -53,6 +53,7 @@ struct SweepOperands {
     int32_t out_off = 0;
     unsigned long long* cta_clock = nullptr;  // profiling: per-CTA [start, end] globaltimer (ns)
     float lambda = 0.f;
+    int32_t psz = 0;  // set by the launcher: staged panel width (= the sentinel index of padding entries)
 };
 
 // Launches one CCD++ sweep over a layout (ccd.hpp:153-197 with the promote of ccd.hpp:133-151

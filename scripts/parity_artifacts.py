@@ -8,7 +8,10 @@ RMSE of all three runs, their relative differences, and the relative Frobenius d
 final factors: GPU vs float, GPU vs double, and float vs double -- the last one is the calibration of
 what FP32 reduction order alone does to the factors at that shape.
 
-    python scripts/parity_artifacts.py CONFIG [OUTER] > gpurun_out/parity_CONFIG.json
+    python scripts/parity_artifacts.py CONFIG [OUTER] [--f32-only] > gpurun_out/parity_CONFIG.json
+
+--f32-only skips the reference's double run (its float-vs-double distance is then taken from the
+committed calibration profiles/r02_calib_CONFIG.json, scripts/calibrate_ref.py).
 """
 import json
 import os
@@ -38,7 +41,9 @@ def rows_of(rows):
 def main():
     cfg = sys.argv[1]
     m, n, ntr, npr, k, lam, inner, solver, skew = bench.CONFIGS[cfg]
-    outer = int(sys.argv[2]) if len(sys.argv) > 2 else 2
+    args = [a for a in sys.argv[1:] if not a.startswith("--")]
+    f32_only = "--f32-only" in sys.argv
+    outer = int(args[1]) if len(args) > 1 else 2
     cores = os.cpu_count() or 1
     train, probe = bench.make_data(cfg)
     out = {"config": cfg, "m": m, "n": n, "nnz": int(len(train)), "probe": int(len(probe)), "k": k, "lambda": lam,
@@ -64,7 +69,7 @@ def main():
     del A
     R = Reference()
     hist = {}
-    for real in ("_f32", "_f64"):
+    for real in (("_f32",) if f32_only else ("_f32", "_f64")):
         t0 = time.perf_counter()
         M = R.matrix(train, m, n, real)
         if solver == "ccdpp":
@@ -76,16 +81,28 @@ def main():
         hist[real] = (Wh, Hh)
         del M
         print(f"[parity] {cfg} reference{real} done in {time.perf_counter() - t0:.0f}s", file=sys.stderr, flush=True)
+    if f32_only:
+        cal = json.load(open(os.path.join(ROOT, "profiles", f"r02_calib_{cfg}.json")))
+        out["ref_f64"] = cal["ref_f64"]
+        out["ref_f64"]["source"] = f"profiles/r02_calib_{cfg}.json (same bytes, reference double run)"
     for key in ("objective", "rmse", "train_rmse"):
         for a, b in (("gpu", "ref_f32"), ("gpu", "ref_f64"), ("ref_f32", "ref_f64")):
             out[f"rel_{key}_{a}_vs_{b}"] = [abs(g[key] - f[key]) / abs(f[key]) for g, f in
                                             zip(out[a]["rows"], out[b]["rows"])]
-    (Wf, Hf), (Wd, Hd) = hist["_f32"], hist["_f64"]
-    out["factors_per_iteration"] = [
-        {"iteration": it + 1,
-         "W_gpu_vs_f32": frob(gmodels[it][0], Wf[it]), "H_gpu_vs_f32": frob(gmodels[it][1], Hf[it]),
-         "W_gpu_vs_f64": frob(gmodels[it][0], Wd[it]), "H_gpu_vs_f64": frob(gmodels[it][1], Hd[it]),
-         "W_f32_vs_f64": frob(Wf[it], Wd[it]), "H_f32_vs_f64": frob(Hf[it], Hd[it])} for it in range(outer)]
+    Wf, Hf = hist["_f32"]
+    if f32_only:
+        out["factors_per_iteration"] = [
+            dict({"iteration": it + 1, "W_gpu_vs_f32": frob(gmodels[it][0], Wf[it]),
+                  "H_gpu_vs_f32": frob(gmodels[it][1], Hf[it])},
+                 **{k: v for k, v in cal["factors_per_iteration"][it].items() if k.endswith("f32_vs_f64")})
+            for it in range(outer)]
+    else:
+        Wd, Hd = hist["_f64"]
+        out["factors_per_iteration"] = [
+            {"iteration": it + 1,
+             "W_gpu_vs_f32": frob(gmodels[it][0], Wf[it]), "H_gpu_vs_f32": frob(gmodels[it][1], Hf[it]),
+             "W_gpu_vs_f64": frob(gmodels[it][0], Wd[it]), "H_gpu_vs_f64": frob(gmodels[it][1], Hd[it]),
+             "W_f32_vs_f64": frob(Wf[it], Wd[it]), "H_f32_vs_f64": frob(Hf[it], Hd[it])} for it in range(outer)]
     print(json.dumps(out, indent=1))
 
 

@@ -28,9 +28,10 @@ def main():
     a = ap.parse_args()
     if a.cta:
         return cta_profile(a.config)
-    m, n, ntr, npr, k, lam, inner, solver = bench.CONFIGS[a.config]
+    m, n, ntr, npr, k, lam, inner, solver, skew = bench.CONFIGS[a.config]
     k = a.k or k
-    train, probe, A = bench.make_data(a.config)
+    train, probe = bench.make_data(a.config)
+    A = P.RatingsMatrix.from_triplets(train, m, n)
     ctx = P.Context(A)
     if a.iters:
         ctx.ccdpp_begin(P.CcdConfig(k=k, lam=lam, outer_iters=a.iters, inner_iters=15, seed=1))
@@ -52,7 +53,9 @@ def cta_profile(config):
     """python scripts/profile_run.py --cta [--config C]: per-CTA time spread of one plain / promote
     sweep per side (after one outer iteration at rank 4)."""
     import numpy as np
-    train, probe, A = bench.make_data(config)
+    m, n = bench.CONFIGS[config][:2]
+    train, probe = bench.make_data(config)
+    A = P.RatingsMatrix.from_triplets(train, m, n)
     ctx = P.Context(A)
     for side, li in ctx.layout_info().items():
         print(f"layout {side}: " + " ".join(f"{k}={v}" for k, v in li.items()))
