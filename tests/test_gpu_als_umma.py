@@ -3,7 +3,7 @@
 The switch is read once per process, so each case runs in a subprocess with the variable set.  Same
 criteria as test_gpu_als.py: per-iteration objective, probe RMSE and train RMSE within 1e-4 of the
 oracle (pinned bit-for-bit to the reference's als_train / ccd_train), factors within 1e-3 relative
-Frobenius; k covers the 4-byte gather path (k % 4 != 0), the 16-byte path, both solver register sets
+Frobenius or twice the reference's float-vs-double distance at that k (k = 40: H 8.9e-4 apart); k covers the 4-byte gather path (k % 4 != 0), the 16-byte path, both solver register sets
 (k > 32) and the item/user-wise CCD Gauss-Seidel epilogue."""
 import json
 import os
@@ -28,17 +28,20 @@ a = O.synth_ratings(943, 1682, 3, 100000, 777)
 train, probe = O.carve_probe(a, 10000, 5)
 A = P.RatingsMatrix.from_triplets(train, 943, 1682)
 OA = O.from_triplets(train, 943, 1682)
+OA64 = O.from_triplets(train, 943, 1682, "_f64")
 if algo == "als":
     model, rep = P.als_train(P.AlsConfig(k=k, lam=0.05, outer_iters=3, seed=1), A, probe)
     W, H, rows = O.als_train(OA, k, 0.05, 3, 1, probe)
+    W64, H64, _ = O.als_train(OA64, k, 0.05, 3, 1, probe, real="_f64")
 else:
     model, rep = P.ccd_train(P.CcdConfig(k=k, lam=0.05, outer_iters=3, inner_iters=1, seed=1), A, probe)
     W, H, rows = O.ccd_train(OA, k, 0.05, 3, 1, probe)
+    W64, H64, _ = O.ccd_train(OA64, k, 0.05, 3, 1, probe, real="_f64")
 def fr(x, y):
     return float(np.linalg.norm(np.float64(x) - np.float64(y)) / np.linalg.norm(np.float64(y)))
 out = {"rel": [[abs(getattr(r, f) - float(g[f])) / abs(float(g[f])) for f in ("objective", "rmse", "train_rmse")]
                for r, g in zip(rep.rows, rows)],
-       "w": fr(model.w, W), "h": fr(model.h, H)}
+       "w": fr(model.w, W), "h": fr(model.h, H), "w_cal": fr(W, W64), "h_cal": fr(H, H64)}
 print(json.dumps(out))
 '''
 
@@ -55,4 +58,6 @@ def test_umma_gram_vs_oracle(algo, k, gram):
     out = json.loads(r.stdout.strip().splitlines()[-1])
     for row in out["rel"]:
         assert max(row) < 1e-4, out
-    assert out["w"] < 1e-3 and out["h"] < 1e-3, out
+    # factors: 1e-3, or twice the oracle's (= the reference's) own float-vs-double distance at this k
+    assert out["w"] <= max(1e-3, 2 * out["w_cal"]), out
+    assert out["h"] <= max(1e-3, 2 * out["h_cal"]), out
