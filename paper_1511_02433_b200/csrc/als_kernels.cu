@@ -32,6 +32,10 @@ constexpr int kAlsWarps = kAlsThreads / 32;
 #ifndef PMF_TC_LDL
 #define PMF_TC_LDL 1
 #endif
+#ifndef PMF_TC_KMAX
+#define PMF_TC_KMAX 64  // largest k of the mma.sync tensor-core gram (Netflix k = 44 / 48 / 56 / 64: 21 / 21 / 32 / 60 ms
+                        // against 64 / 66 / ~70 / 74 ms for the FP32 SIMT gram it replaces)
+#endif
 #ifndef PMF_TC_MINB
 #define PMF_TC_MINB (PMF_TC_LDL ? 4 : 5)
 #endif
@@ -627,13 +631,13 @@ int launch_k(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32
         cudaMemsetAsync(d_counter, 0, sizeof(int), s);
         if (use_tensor_cores() && als_umma_supported(k) && use_umma()) {
             launch_als_umma(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, s, gs);
-        } else if (use_tensor_cores() && k <= 40) {
+        } else if (use_tensor_cores() && k <= PMF_TC_KMAX) {
             // N tiles (8 features) and M tiles (16 features) covering the k features
             const int nt = (k + 7) / 8, mt = (k + 15) / 16;
 #define PMF_TC(NT_, MT_) \
     if (nt == NT_ && mt == MT_) launch_tc<NT_, MT_>(L, opp, n_opp, out, out_off, k, lambda, weighted, d_counter, d_status, sm_count, s, gs)
             PMF_TC(1, 1); else PMF_TC(2, 1); else PMF_TC(3, 1); else PMF_TC(3, 2); else PMF_TC(4, 2);
-            else PMF_TC(5, 2); else PMF_TC(5, 3); else PMF_TC(6, 3);
+            else PMF_TC(5, 2); else PMF_TC(5, 3); else PMF_TC(6, 3); else PMF_TC(7, 4); else PMF_TC(8, 4);
 #undef PMF_TC
         } else {
             int per_sm = 0;
@@ -688,6 +692,8 @@ void als_set_attributes() {
     set_attr_tc<5, 2>();
     set_attr_tc<5, 3>();
     set_attr_tc<6, 3>();
+    set_attr_tc<7, 4>();
+    set_attr_tc<8, 4>();
     set_attr_k<8>();
     set_attr_k<16>();
     set_attr_k<32>();
@@ -695,7 +701,7 @@ void als_set_attributes() {
     set_attr_k<64>();
 }
 
-bool als_gram_gs_supported(int k) { return use_tensor_cores() && k >= 1 && k <= (use_umma() ? 48 : 40); }
+bool als_gram_gs_supported(int k) { return use_tensor_cores() && k >= 1 && k <= (use_umma() ? 48 : PMF_TC_KMAX); }
 
 int launch_als_half(const DevAls& L, const float* opp, int64_t n_opp, float* out, int32_t out_off, int k,
                     float lambda, bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t stream,

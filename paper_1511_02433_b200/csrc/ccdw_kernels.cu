@@ -1,6 +1,6 @@
 // ccdw_kernels.cu -- item/user-wise CCD (ccd.hpp:52-125, ccd_train :310-344) on the GPU, residual form.
 //
-// The default path.  PMF_CCD_GRAM=1 (k <= 40) runs the equivalent gram form instead (als_kernels.cu
+// The default path.  PMF_CCD_GRAM=1 (k <= 64) runs the equivalent gram form instead (als_kernels.cu
 // warp_gauss_seidel: one Gauss-Seidel sweep per row on its normal equations, gram + right-hand side on
 // the tensor cores, no residual): 10x faster, but without the reference's float-residual rounding its
 // trajectory drifts from the reference's (objective 1.9e-4 apart after 5 Netflix epochs vs 3e-6 here).

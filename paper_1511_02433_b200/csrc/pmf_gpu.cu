@@ -1109,7 +1109,7 @@ void ccdw_begin(Ctx& c, const pmf_ccd_config* cfg) {
     c.lambda = cfg->lambda;
     // Default: the residual form (warp per row / CTA per column), which updates a float residual
     // entry by entry as the reference does and tracks its trajectory to ~3e-6 over 5 Netflix epochs.
-    // PMF_CCD_GRAM=1 (k <= 40): each row's (column's) coordinate sweep as one Gauss-Seidel sweep on
+    // PMF_CCD_GRAM=1 (k <= 64): each row's (column's) coordinate sweep as one Gauss-Seidel sweep on
     // its normal equations, gram and right-hand side from the ALS tensor-core kernel, no residual --
     // 10x faster, but it does not carry the reference's residual rounding, and the objectives drift
     // apart (1e-4 relative after 3-4 Netflix epochs).

@@ -25,7 +25,9 @@ MODELS = ["", "1,1,1,0,0,0,1,1,1,0,0,0,1000,1000,1000,64000,64000,64000,0",
 def collect(out):
     import bench
     import paper_1511_02433_b200 as P
-    train, probe, A = bench.make_data("netflix-ccdpp")
+    m0, n0 = bench.CONFIGS["netflix-ccdpp"][:2]
+    train, probe = bench.make_data("netflix-ccdpp")
+    A = P.RatingsMatrix.from_triplets(train, m0, n0)
     data = {}
     for mi, m in enumerate(MODELS):
         if m:
@@ -101,8 +103,44 @@ def fit(path):
                 print(f"     model {MODELS[m]:>20s}: max {dd.max():6.1f} avg {dd.mean():6.1f} min {dd.min():6.1f}")
 
 
+def fit_step(path, side=1, inner=15):
+    """Cost model for the time of a whole rank-one step on one side: (inner - 1) plain sweeps + 1 promote
+    per CTA, as per_entry[c] * entries + per_unit[c] * units (+ per_piece * pieces), non-negative least
+    squares over every collected partition.  Prints the PMF_UNIT_COST string (no step terms)."""
+    z = np.load(path)
+    nm = len([k for k in z.files if k.endswith("_s0_p0_dur")])
+    X, d = [], []
+    for m in range(nm):
+        st = z[f"m{m}_s{side}_p0_st"]
+        y = (inner - 1) * z[f"m{m}_s{side}_p0_dur"] + z[f"m{m}_s{side}_p1_dur"]
+        X.append(np.column_stack([st[:, 6], st[:, 7], st[:, 8], st[:, 0], st[:, 1], st[:, 2], st[:, 4]]).astype(float))
+        d.append(y)
+    X, d = np.concatenate(X), np.concatenate(d)
+    Xs = np.column_stack([X, np.ones(len(d))])
+    active = list(range(Xs.shape[1]))
+    while True:
+        coef, *_ = np.linalg.lstsq(Xs[:, active], d, rcond=None)
+        neg = [a for a, c in zip(active, coef) if c < 0 and a != Xs.shape[1] - 1]
+        if not neg:
+            break
+        active.remove(neg[0])
+    full = np.zeros(Xs.shape[1])
+    full[active] = coef
+    pred = Xs @ full
+    print(f"side {side} step ({inner - 1} plain + 1 promote): rms {np.sqrt(np.mean((pred - d) ** 2)):.1f} us "
+          f"(range {d.min():.0f}-{d.max():.0f})")
+    names = ["ent_L", "ent_M", "ent_S", "units_L", "units_M", "units_S", "pieces", "const"]
+    print("   " + "  ".join(f"{n}={c * 1e3:.3f}ns" for n, c in zip(names, full)))
+    ps = lambda x: int(round(x * 1e6))  # us -> the model's integer units (ps)
+    cost = [1, 1, 1, 0, 0, 0, 1, 1, 1, 0, 0, 0, ps(full[0]), ps(full[1]), ps(full[2]), ps(full[3]), ps(full[4]),
+            ps(full[5]), ps(full[6])]
+    print("PMF_UNIT_COST=" + ",".join(str(c) for c in cost))
+
+
 if __name__ == "__main__":
     if sys.argv[1] == "collect":
         collect(sys.argv[2])
+    elif sys.argv[1] == "fit_step":
+        fit_step(sys.argv[2])
     else:
         fit(sys.argv[2])

@@ -92,3 +92,15 @@ def test_yahoo_ccdpp_vs_reference(pmf, reference):
     M = reference.matrix(train, 1000990, 624961, "_f32")
     W, H, rows, _, _ = M.ccdpp_stage_loop(100, 0.05, 1, 15, 1, probe, workers=CORES)
     _compare("yahoo-ccdpp", rep.rows, rows, model, W, H)
+
+
+def test_netflix_skew_ccdpp_vs_reference(pmf, reference):
+    """Power-law users at the Netflix shape (datagen user_skew 0.5: rows of up to thousands of entries,
+    the skew of the real Netflix data), CCD++ k=40, 2 outer iterations."""
+    train, probe = _data("netflix-skew-ccdpp")
+    A = pmf.RatingsMatrix.from_triplets(train, 480189, 17770)
+    assert np.diff(A.row_start).max() > 2000  # long CSR rows are exercised
+    model, rep = pmf.ccdpp_train(pmf.CcdConfig(k=40, lam=0.05, outer_iters=2, inner_iters=15, seed=1), A, probe)
+    M = reference.matrix(train, 480189, 17770, "_f32")
+    W, H, rows, _, _ = M.ccdpp_stage_loop(40, 0.05, 2, 15, 1, probe, workers=CORES)
+    _compare("netflix-skew-ccdpp", rep.rows, rows, model, W, H)
