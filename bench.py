@@ -141,6 +141,33 @@ def als_flops(N, m, n, k):
     return 2.0 * (2.0 * N * (k * (k + 1) / 2 + k) + (m + n) * (k ** 3 / 6 + k * k))
 
 
+# ALS is issue / latency-bound (ncu: 50-56 % issue slots busy, profiles/r02_ncu_als_*): its roofline object
+# reports the useful FP32-equivalent flops against both compute ceilings it could be held to
+# -- the FP32 SIMT peak (148 SMs x 128 lanes x 2 flops at the 1,965 MHz max clock) and the dense TF32
+# tensor peak measured with tcgen05 (scripts/micro/umma_rate.cu: 2,046 MAC / cycle / SM).
+FP32_SIMT_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+TF32_TENSOR_PEAK_TFLOPS = 148 * 2046 * 2 * 1.965e9 / 1e12
+
+
+def als_roofline(fl, seconds):
+    ach = fl / seconds / 1e12
+    return {"bound": "issue (instruction / latency)", "achieved": round(ach, 2), "unit": "TFLOP/s",
+            "peak": round(FP32_SIMT_PEAK_TFLOPS, 1), "frac": round(ach / FP32_SIMT_PEAK_TFLOPS, 4),
+            "peak_source": "FP32 SIMT peak (148 x 128 x 2 x 1.965 GHz); the dense TF32 tensor peak measured with "
+                           "tcgen05 is also given",
+            "tf32_tensor_peak": round(TF32_TENSOR_PEAK_TFLOPS, 1),
+            "frac_of_tf32_tensor": round(ach / TF32_TENSOR_PEAK_TFLOPS, 4),
+            "flops_per_iter": fl, "note": "useful FP32-equivalent flops: 2 [2N(k(k+1)/2 + k) + (m + n)(k^3/6 + k^2)]"}
+
+
+def ccd_epoch_roofline(N, k, seconds, hbm):
+    """item/user-wise CCD: SURVEY 8(d) algorithmic bytes 8N per coordinate t per side."""
+    b = 2 * k * 8 * N
+    return {"bound": "hbm", "achieved": round(b / seconds / 1e9, 1), "unit": "GB/s", "peak": hbm,
+            "frac": round(b / seconds / 1e9 / hbm, 4), "algorithmic_bytes_per_epoch": b,
+            "note": "latency-bound (per-coordinate dependent gathers); the column sweep claims columns longest first"}
+
+
 def barrier(dist):
     if dist:
         import torch.distributed as td
@@ -283,9 +310,7 @@ def run_ours(args, rank, world, dist):
     if solver == "ccdpp":
         res["roofline"] = ccdpp_roofline(ctx, iterate, N, m, n, k, inner, value, hbm, args.config)
     else:
-        fl = als_flops(N, m, n, k)
-        res["roofline"] = {"bound": "fp32/tensor", "achieved": round(fl / value / 1e12, 2), "unit": "TFLOP/s",
-                           "note": "FP32-equivalent useful flops (SURVEY 8d) / time"}
+        res["roofline"] = als_roofline(als_flops(N, m, n, k), value)
     res.update(ctx=ctx, nccl_id=nccl_id, A=A, probe=probe, train=train)
     return res
 
@@ -380,6 +405,7 @@ def side_gpu(P, cfg_name, warm=1, steps=3, profile=False):
     else:
         fl = als_flops(A.nnz(), m, n, k)
         out["useful_tflops"] = round(fl / v / 1e12, 2)
+        out["roofline"] = als_roofline(fl, v)
     ctx.close()
     return out, train, probe, A
 
@@ -421,13 +447,15 @@ def extras_n1(args, res):
         fl = als_flops(res["A"].nnz(), m, n, k)
         ex["als"] = {"config": "netflix-als", "value": float(np.mean(ts)), "unit": "s/outer-iter",
                      "launches_per_iter": ctx.launch_count(), "objective": o, "probe_rmse": r,
-                     "useful_tflops": round(fl / float(np.mean(ts)) / 1e12, 2), "flops_per_iter": fl}
+                     "useful_tflops": round(fl / float(np.mean(ts)) / 1e12, 2), "flops_per_iter": fl,
+                     "roofline": als_roofline(fl, float(np.mean(ts)))}
         # item/user-wise CCD epochs (residual form) on the same context
         ctx.ccd_begin(P.CcdConfig(k=k, lam=lam, outer_iters=1, inner_iters=1, seed=MODEL_SEED))
         ctx.ccd_iterate(1)
         tc = list(ctx.ccd_iterate(3))
         ex["ccd"] = {"metric": "sec/epoch item/user-wise CCD k=40 Netflix shape (residual form)",
-                     "value": float(np.mean(tc)), "unit": "s/epoch", "objective": ctx.metrics()[0]}
+                     "value": float(np.mean(tc)), "unit": "s/epoch", "objective": ctx.metrics()[0],
+                     "roofline": ccd_epoch_roofline(res["A"].nnz(), k, float(np.mean(tc)), peaks().get("hbm_gbs", 6544.7))}
         # RatingsMatrix::from_triplets on the GPU vs the host build (same bytes out)
         trn = res["train"]
         P.RatingsMatrix.from_triplets(trn[:100000], m, n, device=True)

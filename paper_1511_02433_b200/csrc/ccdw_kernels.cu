@@ -85,6 +85,13 @@ __global__ void ccd_rows_kernel(const int64_t* __restrict__ row_start, const int
                 jj[c] = p < e ? col_of[p] : 0;
             }
         }
+        // cached rows: the gathered h of coordinate t + 1 are loaded while t is reduced (its h only
+        // depends on the fixed H), so the L2 gathers are off the t-to-t dependency chain
+        float hn[kRowCache];
+        if (cached) {
+#pragma unroll
+            for (int c = 0; c < kRowCache; ++c) hn[c] = b + lane + 32 * c < e ? H[static_cast<int64_t>(jj[c]) * k] : 0.f;
+        }
         for (int t = 0; t < k; ++t) {
             const float wit = W[i * k + t];
             float num = 0.f, den = 0.f;
@@ -92,8 +99,9 @@ __global__ void ccd_rows_kernel(const int64_t* __restrict__ row_start, const int
             if (cached) {
 #pragma unroll
                 for (int c = 0; c < kRowCache; ++c) {
+                    hc[c] = hn[c];
                     const bool in = b + lane + 32 * c < e;
-                    hc[c] = in ? H[static_cast<int64_t>(jj[c]) * k + t] : 0.f;
+                    if (t + 1 < k) hn[c] = in ? H[static_cast<int64_t>(jj[c]) * k + t + 1] : 0.f;
                     if (in) {
                         num = __fadd_rn(num, __fmul_rn(__fadd_rn(r[c], __fmul_rn(wit, hc[c])), hc[c]));
                         den = __fadd_rn(den, __fmul_rn(hc[c], hc[c]));
@@ -172,6 +180,110 @@ ccd_cols_kernel(const int64_t* __restrict__ col_start, const int32_t* __restrict
     }
 }
 
+// H sweep, longest columns first: CTAs of kColThreadsL claim columns from a counter over col_order (LPT;
+// the popular columns hold up to ~5 % of the entries each), and gather w_it from the column-major copy
+// WT (k x m), so that the dense row ranges of long columns read coalesced.  One pass per coordinate t:
+// the pass of t applies the residual shift of t - 1 (R -= (z - h_j,t-1) w_i,t-1, the reference's
+// ccd_apply_s arithmetic, deferred) and accumulates the sums of t; a last pass applies the shift of k - 1.
+constexpr int kColThreadsL = 1024;
+__global__ void __launch_bounds__(kColThreadsL)
+ccd_cols_lpt_kernel(const int64_t* __restrict__ col_start, const int32_t* __restrict__ row_of, float* __restrict__ R,
+                    const float* __restrict__ WT, float* __restrict__ H, int32_t n, int32_t m, int k, float lambda,
+                    const int32_t* __restrict__ col_order, int* __restrict__ counter) {
+    __shared__ float s_num[kColThreadsL / 32], s_den[kColThreadsL / 32];
+    __shared__ float s_z;
+    __shared__ int s_j;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (;;) {
+        if (threadIdx.x == 0) s_j = atomicAdd(counter, 1);
+        __syncthreads();
+        const int jj = s_j;
+        __syncthreads();
+        if (jj >= n) break;
+        const int32_t j = col_order[jj];
+        const int64_t b = col_start[j], e = col_start[j + 1];
+        float dprev = 0.f;
+        for (int t = 0; t <= k; ++t) {
+            const bool last = t == k;
+            const float hjt = last ? 0.f : H[static_cast<int64_t>(j) * k + t];
+            const float* wt = WT + static_cast<int64_t>(t) * m;
+            const float* wp = WT + static_cast<int64_t>(t - 1) * m;
+            float num = 0.f, den = 0.f;
+            // four entries per thread per step, all loads issued before their use (long columns stream
+            // through one CTA: the dependent row -> w gathers need several in flight per thread)
+            constexpr int U = 4;
+            for (int64_t q0 = b + threadIdx.x; q0 < e; q0 += U * kColThreadsL) {
+                int32_t iu[U];
+                float ru[U], pu[U], wu[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t q = q0 + static_cast<int64_t>(u) * kColThreadsL;
+                    iu[u] = q < e ? row_of[q] : 0;
+                    ru[u] = q < e ? R[q] : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    pu[u] = t > 0 ? wp[iu[u]] : 0.f;
+                    wu[u] = last ? 0.f : wt[iu[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int64_t q = q0 + static_cast<int64_t>(u) * kColThreadsL;
+                    if (q >= e) continue;
+                    float r = ru[u];
+                    if (t > 0) {
+                        r = __fsub_rn(r, __fmul_rn(dprev, pu[u]));
+                        R[q] = r;
+                    }
+                    if (!last) {
+                        num = __fadd_rn(num, __fmul_rn(__fadd_rn(r, __fmul_rn(wu[u], hjt)), wu[u]));
+                        den = __fadd_rn(den, __fmul_rn(wu[u], wu[u]));
+                    }
+                }
+            }
+            if (last) break;
+            warp_sum2(num, den);
+            if (lane == 0) {
+                s_num[warp] = num;
+                s_den[warp] = den;
+            }
+            __syncthreads();
+            if (warp == 0) {
+                num = s_num[lane];
+                den = s_den[lane];
+                warp_sum2(num, den);
+                if (lane == 0) {
+                    const float dt = __fadd_rn(lambda, den);
+                    s_z = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+                }
+            }
+            __syncthreads();
+            const float z = s_z;
+            dprev = __fsub_rn(z, hjt);
+            if (threadIdx.x == 0) H[static_cast<int64_t>(j) * k + t] = z;
+            __syncthreads();  // s_z read by every thread before the next t overwrites it
+        }
+    }
+}
+
+// WT (k x m, column-major) <- W (m x k, row-major): 32 x 32 tiles through shared memory
+__global__ void ccd_transpose_kernel(const float* __restrict__ W, float* __restrict__ WT, int32_t m, int k) {
+    __shared__ float tile[32][33];
+    const int64_t i0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int t0 = blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t i = i0 + r;
+        const int t = t0 + threadIdx.x;
+        tile[r][threadIdx.x] = (i < m && t < k) ? W[i * k + t] : 0.f;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int t = t0 + r;
+        const int64_t i = i0 + threadIdx.x;
+        if (t < k && i < m) WT[static_cast<int64_t>(t) * m + i] = tile[threadIdx.x][r];
+    }
+}
+
 // R = A - W H^T from scratch (a warp per row; t ascending, each product rounded before the subtract):
 // the residual of a model installed with set_model (residual_from + the writebacks' arithmetic).
 __global__ void ccd_residual_kernel(const int64_t* __restrict__ row_start, const int32_t* __restrict__ col_of,
@@ -213,7 +325,13 @@ int launch_ccd_epoch(const CcdWs& ws, float* W, float* H, int k, float lambda, c
         ccd_gather_kernel<<<148 * 16, 256, 0, s>>>(ws.R_col, ws.R_row, ws.csc2csr, ws.nnz);  // set_from_row
         ++launched;
     }
-    if (ws.n > 0) {
+    if (ws.n > 0 && ws.WT) {
+        ccd_transpose_kernel<<<dim3((ws.m + 31) / 32, (k + 31) / 32), dim3(32, 8), 0, s>>>(W, ws.WT, ws.m, k);
+        cudaMemsetAsync(ws.counter, 0, sizeof(int), s);
+        ccd_cols_lpt_kernel<<<148, kColThreadsL, 0, s>>>(ws.col_start, ws.row_of, ws.R_col, ws.WT, H, ws.n, ws.m, k,
+                                                         lambda, ws.col_order, ws.counter);
+        launched += 2;
+    } else if (ws.n > 0) {
         ccd_cols_kernel<<<148 * 8, kColThreads, 0, s>>>(ws.col_start, ws.row_of, ws.R_col, W, H, ws.n, k, lambda);
         ++launched;
     }

@@ -115,6 +115,9 @@ struct CcdWs {
     float* R_col = nullptr;      // residual, CSC order
     int32_t* csr2csc = nullptr;  // position maps (the reference's xlinks)
     int32_t* csc2csr = nullptr;
+    float* WT = nullptr;           // k x m column-major copy of W for the H sweep (coalesced gathers)
+    int32_t* col_order = nullptr;  // columns longest first (the H sweep claims them in this order)
+    int* counter = nullptr;
 };
 void launch_ccd_xlinks(const int64_t* row_start, const int32_t* col_of, const int64_t* col_start,
                        const int32_t* row_of, int32_t m, int32_t* csr2csc, int32_t* csc2csr, cudaStream_t s);

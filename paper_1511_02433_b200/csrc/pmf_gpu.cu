@@ -17,6 +17,7 @@
 #include <future>
 #include <map>
 #include <mutex>
+#include <numeric>
 #include <thread>
 #include <memory>
 #include <random>
@@ -1144,6 +1145,16 @@ void ccdw_begin(Ctx& c, const pmf_ccd_config* cfg) {
         CUDA_TRY(cudaMemcpyAsync(w.R_col, c.als_csc.val, sizeof(float) * c.nnz, cudaMemcpyDeviceToDevice, c.stream));
     }
     launch_ccd_xlinks(w.row_start, w.col_of, w.col_start, w.row_of, w.m, w.csr2csc, w.csc2csr, c.stream);
+    {  // H sweep: W column-major copy, columns longest first
+        w.WT = c.ccdw_mem.alloc<float>(static_cast<size_t>(std::max<int32_t>(c.m, 1)) * c.k, false);
+        std::vector<int32_t> order(c.n);
+        std::iota(order.begin(), order.end(), 0);
+        const auto& cs = c.col_start_local;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](int32_t a, int32_t b) { return cs[a + 1] - cs[a] > cs[b + 1] - cs[b]; });
+        w.col_order = c.ccdw_mem.upload(order, c.stream, &c.h2d);
+        w.counter = c.ccdw_mem.alloc<int>(1);
+    }
     c.W = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_m + 1) * c.k);
     c.H = c.model_mem.alloc<float>(static_cast<size_t>(c.ext_n + 1) * c.k);
     const auto H = init_items_host(c.n, cfg->k, cfg->seed);  // model.hpp:86-93

@@ -1,2 +1,2 @@
 mkdir -p gpurun_out
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:als_umma -c 1 -o gpurun_out/prof_umma -f python bench.py --config ${1:-netflix-als} --no-extra --no-cpu-baseline --no-e2e --steps 1 --warmup 1 > gpurun_out/ncu_umma.log 2>&1
+timeout 400 ncu --set full --import-source on --clock-control none -k regex:als_gram_tc -c 2 -o gpurun_out/prof_als -f python scripts/als_k_check.py ${1:-40} 1 > gpurun_out/ncu_als.log 2>&1
