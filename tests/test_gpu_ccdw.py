@@ -59,6 +59,28 @@ def test_ccd_long_rows_vs_oracle(pmf, oracle):
     assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
 
 
+@pytest.mark.slow
+def test_ccd_long_columns_vs_oracle(pmf, oracle):
+    """Columns of more than 32K entries take the cluster kernel (8 CTAs per column, DSMEM reduction)."""
+    rng = np.random.default_rng(4)
+    m, n = 60000, 50
+    rows, cols = [], []
+    for j in range(n):
+        cnt = 50000 if j % 5 == 0 else int(rng.integers(1, 3000))   # 10 columns above the threshold
+        rows.append(rng.choice(m, cnt, replace=False)); cols.append(np.full(cnt, j))
+    i = np.concatenate(rows); j = np.concatenate(cols)
+    t = np.zeros(i.size, dtype=[("user", "<i4"), ("item", "<i4"), ("rating", "<f4")])
+    t["user"], t["item"], t["rating"] = i, j, rng.integers(1, 6, i.size)
+    A = pmf.RatingsMatrix.from_triplets(t, m, n)
+    O = oracle.from_triplets(t, m, n)
+    model, rep = pmf.ccd_train(pmf.CcdConfig(k=6, lam=0.05, outer_iters=3, inner_iters=1, seed=2), A)
+    W, H, rws = oracle.ccd_train(O, 6, 0.05, 3, 2)
+    for r, g in zip(rep.rows, rws):
+        assert rel(r.objective, g["objective"]) < 1e-4
+        assert rel(r.train_rmse, g["train_rmse"]) < 1e-4
+    assert frob_rel(model.w, W) < 1e-3 and frob_rel(model.h, H) < 1e-3
+
+
 def test_ccd_paths_vs_oracle(pmf, oracle, ml100k, monkeypatch):
     # default: the residual kernels; PMF_CCD_GRAM=1 (k <= 40): gram + Gauss-Seidel; k > 40 always residual
     train, probe = ml100k
