@@ -212,7 +212,11 @@ __device__ __forceinline__ void mma_tf32(float (&d)[4], uint32_t a0, uint32_t a1
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
 }
 
-template <int NT, int MT>
+// G4: the gather4 staging only (tma == 2, the B200 default; the other stagings stay behind the runtime
+// `tma` of G4 = false).  GSW: the item/user-wise CCD Gauss-Seidel epilogue instead of the ALS solve.  Both
+// are compile-time so the hot kernel carries one staging and one epilogue (smaller code: the W side
+// stalled on instruction fetch with all of them in one body).
+template <int NT, int MT, bool G4, bool GSW>
 __global__ void __launch_bounds__(kTcThreads, PMF_TC_MINB)
 als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_t* __restrict__ idx,
                    const float* __restrict__ val, const float* __restrict__ opp, float* __restrict__ out,
@@ -233,6 +237,8 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
     float* sval = X + T::WARP_FLOATS - 32;
     uint64_t* bar = &s_bar[warp];
     uint32_t phase = 0;
+    if (G4) tma = 2;
+    else if (tma == 2) tma = 1;
     if (tma) {
         // TMA rows (4k bytes each) leave columns [k, KS) untouched: zero them here (and per unit after
         // the aliased gram has overwritten them)
@@ -258,7 +264,7 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
 #pragma unroll
         for (int t = 0; t < MT; ++t) accr[t][0] = accr[t][1] = accr[t][2] = accr[t][3] = 0.f;
         float rhs0 = 0.f, rhs1 = 0.f;
-        if (tma == 1 && KS != k) {
+        if (!G4 && tma == 1 && KS != k) {
             // per-row bulk copies write k columns: re-zero the padding columns the previous unit's
             // gram (aliasing the stage) overwrote
             __syncwarp();
@@ -268,7 +274,7 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
             const int cnt = min(32, U.len - base);
             const int cnt8 = (cnt + 7) & ~7;
             __syncwarp();
-            if (tma == 2) {
+            if (G4) {
                 // TMA gather4: one elected lane issues cnt8 / 4 tensor copies of 4 rows each (rows past
                 // cnt use an out-of-bounds row coordinate and arrive zero-filled); X's row stride is k
                 const int row = lane < cnt ? idx[U.e0 + base + lane] : 0x7fffffff;
@@ -430,7 +436,7 @@ als_gram_tc_kernel(const Unit* __restrict__ units, int32_t n_units, const int32_
         }
         __syncwarp();
         float* dst = out + static_cast<int64_t>(out_off + U.o) * k;
-        if (gs) {  // item/user-wise CCD: one coordinate sweep from the current row
+        if (GSW) {  // item/user-wise CCD: one coordinate sweep from the current row
             float x0 = lane < k ? dst[lane] : 0.f, x1 = lane + 32 < k ? dst[lane + 32] : 0.f;
             warp_gauss_seidel<KMAX, GS>(G, k, rhs0, rhs1, x0, x1);
             if (lane < k) dst[lane] = x0;
@@ -610,16 +616,25 @@ void launch_tc(const DevAls& L, const float* opp, int64_t n_opp, float* out, int
                bool weighted, int* d_counter, int* d_status, int sm_count, cudaStream_t s, bool gs) {
     const size_t sm = smem_for_tc<NT, MT>();
     int per_sm = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, als_gram_tc_kernel<NT, MT>, kTcThreads, sm);
-    const int blocks = std::max(1, std::min<int>(per_sm * sm_count, (L.n_units + kTcWarps - 1) / kTcWarps));
     // TMA row staging needs 16-byte rows (k % 4 == 0; the factor base is cudaMalloc-aligned)
     const int mode = als_tma_mode();
     int tma = mode != 0 && k % 4 == 0 && (reinterpret_cast<uintptr_t>(opp) & 15) == 0 ? 1 : 0;
     alignas(64) CUtensorMap map{};
     if (tma && mode == 2 && k == TcGeo<NT, MT>::KS && make_rows_map(&map, opp, n_opp, k)) tma = 2;
-    als_gram_tc_kernel<NT, MT><<<blocks, kTcThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off,
-                                                                k, lambda, weighted ? 1 : 0, L.partial, d_counter,
-                                                                d_status, tma, gs ? 1 : 0, map);
+    auto go = [&](auto kern) {
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kTcThreads, sm);
+        const int blocks = std::max(1, std::min<int>(per_sm * sm_count, (L.n_units + kTcWarps - 1) / kTcWarps));
+        kern<<<blocks, kTcThreads, sm, s>>>(L.units, L.n_units, L.idx, L.val, opp, out, out_off, k, lambda,
+                                            weighted ? 1 : 0, L.partial, d_counter, d_status, tma, gs ? 1 : 0, map);
+    };
+    if (tma == 2) {
+        if (gs) go(als_gram_tc_kernel<NT, MT, true, true>);
+        else go(als_gram_tc_kernel<NT, MT, true, false>);
+    } else {
+        if (gs) go(als_gram_tc_kernel<NT, MT, false, true>);
+        else go(als_gram_tc_kernel<NT, MT, false, false>);
+    }
 }
 
 template <int KMAX>
@@ -678,8 +693,11 @@ void set_attr_k() {
 
 template <int NT, int MT>
 void set_attr_tc() {
-    cudaFuncSetAttribute(als_gram_tc_kernel<NT, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem_for_tc<NT, MT>()));
+    const int bytes = static_cast<int>(smem_for_tc<NT, MT>());
+    cudaFuncSetAttribute(als_gram_tc_kernel<NT, MT, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(als_gram_tc_kernel<NT, MT, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(als_gram_tc_kernel<NT, MT, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    cudaFuncSetAttribute(als_gram_tc_kernel<NT, MT, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
 }
 
 void als_set_attributes() {
