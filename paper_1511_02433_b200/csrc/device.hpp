@@ -32,6 +32,8 @@ struct DevSweep {
     int* gcnt = nullptr;            // 4 per piece (class / chunk counters) + 1 (CTAs done): work stealing
     bool flat = false;              // segmented-stream layout (flat_kernels.cu)
     FlatChunk* chunks = nullptr;
+    int32_t* uinfo = nullptr;       // flat: per unit partial slot, or -(output + 1) (direct write)
+    int32_t* uout = nullptr;        // flat: per unit output
     uint32_t* tailbits = nullptr;
     bool promote_fused = true;      // else: rmw_sub residual sub-passes + a plain sweep
     int32_t rmw_sub = 1, sub_width = 0;

@@ -97,29 +97,32 @@ __device__ __forceinline__ void st8(float* p, const float* r) {
 // fields are kept as they are and only combined where they are used (in flat_block), so a warp does
 // not stall on the descriptor loads of the chunk after next while it streams the current one.
 struct ChunkInfo {
-    int slotA, oA;  // unit ua + lane: partial slot (< 0: direct write of output o)
-    int slotB, oB;  // unit ua + 32 + lane
+    int infoA, oA;  // unit ua + lane: partial slot, or -(output + 1) for a direct write; output
+    int infoB, oB;  // unit ua + 32 + lane
     float facA, facB;  // residual passes: the units' output factors
     uint32_t tw;    // tail word w0 + lane
 };
 
+// Unit descriptors of a flat layout as separate 4-byte streams (uinfo: slot or -(output + 1); uout:
+// output, read by the residual passes only): the plain sweeps read 4 bytes per unit instead of the
+// 16-byte Unit (12M units per Yahoo-Music sweep).
 template <int FM>
-__device__ __forceinline__ ChunkInfo chunk_info(const FlatChunk& ch, const Unit* __restrict__ units,
-                                                const uint32_t* __restrict__ tb, const SweepOperands& op) {
+__device__ __forceinline__ ChunkInfo chunk_info(const FlatChunk& ch, const int32_t* __restrict__ uinfo,
+                                                const int32_t* __restrict__ uout, const uint32_t* __restrict__ tb,
+                                                const SweepOperands& op) {
     constexpr bool kWrite = FM != kFPlain;
     const int lane = threadIdx.x & 31;
     ChunkInfo ci{0, 0, 0, 0, 0.f, 0.f, 0u};
     const int last = max(ch.ub - 1, 0);
-    const int2 a = *reinterpret_cast<const int2*>(&units[min(ch.ua + lane, last)].o);  // clamped: no branch
-    const int2 b = *reinterpret_cast<const int2*>(&units[min(ch.ua + 32 + lane, last)].o);
-    ci.oA = a.x;
-    ci.slotA = a.y;
-    ci.oB = b.x;
-    ci.slotB = b.y;
+    const int ua = min(ch.ua + lane, last), ub = min(ch.ua + 32 + lane, last);  // clamped: no branch
+    ci.infoA = uinfo[ua];
+    ci.infoB = uinfo[ub];
     if (kWrite) {
+        ci.oA = uout[ua];
+        ci.oB = uout[ub];
         const float* f = FM == kFDemote ? op.oa : op.ob;
-        ci.facA = f[op.out_off + a.x];
-        ci.facB = f[op.out_off + b.x];
+        ci.facA = f[op.out_off + ci.oA];
+        ci.facB = f[op.out_off + ci.oB];
     }
     const int w0 = ch.v0 >> 5;
     ci.tw = __ldg(tb + w0 + min(lane, kFlatChunkVectors / 32 + 1));
@@ -139,8 +142,7 @@ __device__ __forceinline__ void flat_block(float (&r)[16], const uint32_t (&ix)[
     const int lane = threadIdx.x & 31;
     const uint32_t lt = (1u << lane) - 1u;
     const int v0 = ch.v0, v1 = ch.v1;
-    // slot, or -(output + 1): direct write
-    const int infoA = ci.slotA >= 0 ? ci.slotA : -(ci.oA + 1), infoB = ci.slotB >= 0 ? ci.slotB : -(ci.oB + 1);
+    const int infoA = ci.infoA, infoB = ci.infoB;  // slot, or -(output + 1): direct write
     const int w0 = v0 >> 5;
     const uint32_t tw = ci.tw;
     const int lv = vb + 4 * lane;
@@ -316,7 +318,7 @@ struct FlatClaim {
 
 template <int FM, bool CSR>
 __global__ void __launch_bounds__(kFlatThreads, 1)
-flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, const int32_t* __restrict__ piece_start,
+flat_kernel(const int32_t* __restrict__ uinfo, const int32_t* __restrict__ uout, const Piece* __restrict__ pieces, const int32_t* __restrict__ piece_start,
             const int32_t* __restrict__ panel_base, const FlatChunk* __restrict__ chunks,
             const uint32_t* __restrict__ tb, const uint16_t* __restrict__ idx, float* __restrict__ R,
             float2* __restrict__ partial, SweepOperands op, const float* __restrict__ gsrc, int32_t panel_size,
@@ -400,9 +402,9 @@ flat_kernel(const Unit* __restrict__ units, const Piece* __restrict__ pieces, co
         int c1 = cl.next(), c2 = cl.next();
         FlatChunk ch1 = c1 < cend ? chunks[c1] : none;
         FlatChunk ch2 = c2 < cend ? chunks[c2] : none;
-        ChunkInfo ci1 = chunk_info<FM>(ch1, units, tb, op);
+        ChunkInfo ci1 = chunk_info<FM>(ch1, uinfo, uout, tb, op);
         while (c1 < cend) {
-            const ChunkInfo ci2 = chunk_info<FM>(ch2, units, tb, op);
+            const ChunkInfo ci2 = chunk_info<FM>(ch2, uinfo, uout, tb, op);
             const int c3 = cl.next();
             const FlatChunk ch3 = c3 < cend ? chunks[c3] : none;
             flat_chunk<FM, CSR>(ch1, ci1, idx, R, partial, op, smem, panel_size);
@@ -450,7 +452,7 @@ void launch_flat_mode(const DevSweep& L, const SweepOperands& op, const float* g
                       cudaStream_t s) {
     const size_t smem = static_cast<size_t>(((L.panel_size + 1) + 3) & ~3) * sizeof(float);
     flat_kernel<FM, CSR><<<L.ctas, kFlatThreads, smem, s>>>(
-        L.units, L.pieces, L.piece_start, L.panel_base, L.chunks, L.tailbits, static_cast<const uint16_t*>(L.idx),
+        L.uinfo, L.uout, L.pieces, L.piece_start, L.panel_base, L.chunks, L.tailbits, static_cast<const uint16_t*>(L.idx),
         L.R, L.partial, op, gsrc, L.panel_size, steal ? L.gcnt : nullptr, L.n_pieces, flat_restage_min());
 }
 

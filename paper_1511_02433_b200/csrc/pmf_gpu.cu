@@ -502,6 +502,13 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     if (L.flat) {
         D.chunks = c.mem.upload(L.chunks, c.stream, &c.h2d);
         D.tailbits = c.mem.upload(L.tailbits, c.stream, &c.h2d);
+        std::vector<int32_t> info(L.units.size()), out(L.units.size());
+        for (size_t u = 0; u < L.units.size(); ++u) {
+            out[u] = L.units[u].o;
+            info[u] = L.units[u].slot >= 0 ? L.units[u].slot : -(L.units[u].o + 1);
+        }
+        D.uinfo = c.mem.upload(info, c.stream, &c.h2d);
+        D.uout = c.mem.upload(out, c.stream, &c.h2d);
     }
     D.ctas = L.ctas;
     D.n_slots = L.n_slots;
