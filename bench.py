@@ -470,6 +470,22 @@ def extras_n1(args, res):
         ex["ingest"] = {"from_triplets_gpu_s": round(t_gpu, 3), "from_triplets_host_s": round(t_host, 3),
                         "host_threads": cores, "bitwise_equal": bool(same), "nnz": int(len(trn))}
         del Ag, Ah
+        # triplets -> a ready device context: the host matrix + pmf_ctx_create (layouts built on the host,
+        # uploaded) vs pmf_ctx_create_from_triplets (CSR / CSC built and kept on the device, layout streams
+        # filled there)
+        P.Context.from_triplets(trn[:100000], m, n).close()
+        t0 = time.perf_counter()
+        cd = P.Context.from_triplets(trn, m, n)
+        t_cdev = time.perf_counter() - t0
+        li_dev = cd.layout_info()
+        cd.close()
+        t0 = time.perf_counter()
+        ch = P.Context(P.RatingsMatrix.from_triplets(trn, m, n))
+        t_chost = time.perf_counter() - t0
+        li_host = ch.layout_info()
+        ch.close()
+        ex["ingest"].update({"ctx_from_triplets_device_s": round(t_cdev, 3), "ctx_via_host_matrix_s": round(t_chost, 3),
+                             "same_layouts": li_dev == li_host})
     res["ctx"].close()
     if args.config == "netflix-ccdpp" and not args.quick:
         # configs[4]: Yahoo-Music CCD++ k=100; power-law users at Netflix shape

@@ -134,6 +134,13 @@ typedef struct pmf_ctx pmf_ctx;
 
 /* Uploads CSR+CSC and builds the device layouts on `device` (-1 = current). */
 pmf_status pmf_ctx_create(const pmf_matrix_view* a, int32_t device, pmf_ctx** out);
+/* The same straight from triplets (RatingsMatrix::from_triplets + the context, sparse.hpp:73-149):
+ * the CSR / CSC are built on the device and stay there; only the offsets and per-(panel, output)
+ * segment lengths come to the host, which builds the layouts' structure; the residual / index streams
+ * are filled on the device.  Same validation errors as pmf_matrix_from_triplets; layouts bitwise those
+ * of pmf_ctx_create on the same matrix.  One device (world 1). */
+pmf_status pmf_ctx_create_from_triplets(const pmf_triplet* triplets, int64_t nnz, int32_t m, int32_t n,
+                                        int32_t device, pmf_ctx** out);
 pmf_status pmf_ctx_destroy(pmf_ctx* ctx);
 
 /* CCD++: W = 0, H = init_random_items(seed) (model.hpp:86-93), R = A. */

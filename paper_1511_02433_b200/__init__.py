@@ -110,6 +110,7 @@ _SIGS = {
     "pmf_rmse": ([_P, _P, C.c_int32, C.c_int32, C.c_int32, _P, C.c_int64, _P], C.c_int),
     "pmf_objective": ([_P, _P, _P, C.c_int32, C.c_double, _P], C.c_int),
     "pmf_ctx_create": ([_P, C.c_int32, _P], C.c_int),
+    "pmf_ctx_create_from_triplets": ([_P, C.c_int64, C.c_int32, C.c_int32, C.c_int32, _P], C.c_int),
     "pmf_ctx_create_dist": ([_P, C.c_int32, C.c_int32, C.c_int32, _P, _P], C.c_int),
     "pmf_ctx_create_group": ([_P, C.c_int32, _P, _P], C.c_int),
     "pmf_ctx_destroy": ([_P], C.c_int),
@@ -696,6 +697,16 @@ def top_n(model: FactorModel, *args):
 # resident context
 # ---------------------------------------------------------------------------------------------
 
+class _Shape:
+    """m, n, nnz() of a context built from triplets (no host matrix)."""
+
+    def __init__(self, m, n, nnz):
+        self.m, self.n, self._nnz = m, n, nnz
+
+    def nnz(self):
+        return self._nnz
+
+
 class Context:
     """Matrix resident in HBM (pmf_ctx); CCD++ / ALS state, metrics and model I/O."""
 
@@ -719,6 +730,21 @@ class Context:
             idb = (C.c_uint8 * 128).from_buffer_copy(nccl_id)
             _check(lib.pmf_ctx_create_dist(a.view(), device, rank, world, idb, C.byref(self.h)))
         self.k = 0
+
+    @classmethod
+    def from_triplets(cls, triplets, m: int, n: int, device: int = -1) -> "Context":
+        """RatingsMatrix.from_triplets + Context in one step with the matrix built on the device
+        (pmf_ctx_create_from_triplets): the CSR / CSC never travel back to the host.  Same errors as
+        from_triplets; layouts (and so every result) bitwise those of Context(RatingsMatrix...)."""
+        if m < 0 or n < 0:
+            raise ValueError("matrix dimensions must be non-negative")
+        t = _as_triplets(triplets)
+        self = cls.__new__(cls)
+        self.a = _Shape(m, n, len(t))
+        self.h = C.c_void_p()
+        _check(lib.pmf_ctx_create_from_triplets(_ptr(t), len(t), m, n, device, C.byref(self.h)))
+        self.k = 0
+        return self
 
     def close(self):
         if self.h:

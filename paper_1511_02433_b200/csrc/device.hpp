@@ -188,6 +188,17 @@ int launch_als_big(const DevAls& L, const float* opp, float* out, int32_t out_of
 void launch_cholesky_big(float* a, float* x, int batch, int k, int* d_status, int sm_count, float* gscratch,
                          cudaStream_t s);
 void als_set_attributes();
+// Device-built sweep layouts (layout_device.cu): per-(panel, output) segment lengths of a device CSR /
+// CSC, the padded residual / index streams filled from it (delta: per segment, padded minus source
+// position; layout.hpp SweepLayout::seg_delta), and the rmw sub-panel split points of every unit.
+void seg_count_device(const int64_t* start, const int32_t* idx, int32_t n_out, int32_t pg, int32_t np,
+                      int32_t* seg_len, cudaStream_t s);
+void layout_fill_device(const int64_t* start, const int32_t* idx, const float* val, int32_t n_out, int64_t nnz,
+                        int32_t pg, int32_t np, const int64_t* delta, bool idx16, int32_t sentinel, int64_t n_entries,
+                        void* out_idx, float* out_val, cudaStream_t s);
+void usplit_device(const Unit* units, const int32_t* real, int64_t nu, const uint16_t* idx, int S, int32_t sub_width,
+                   uint16_t* out, cudaStream_t s);
+
 // Batched Cholesky factor + solve of `batch` k*k row-major systems in place.
 void launch_cholesky_batched(float* a, float* x, int batch, int k, int* d_status,
                              cudaStream_t stream);

@@ -153,7 +153,7 @@ static void parallel_for_outputs(const int64_t* start, int32_t out_begin, int32_
 SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const float* val,
                                int32_t out_begin, int32_t out_end, const int32_t* gmap,
                                int32_t gat_extent, int stage_arrays, int smem_budget_bytes,
-                               int ctas, bool allow_idx16) {
+                               int ctas, bool allow_idx16, const SegCounter* dev) {
     static const bool verbose = std::getenv("PMF_VERBOSE") != nullptr;
     auto clk = [] { return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count(); };
     double tp[8] = {clk()};
@@ -189,6 +189,10 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     L.n_real = nnz_side;
     // panel of gather index g, tracked incrementally along an output's ascending indices
     auto count_segments = [&](int32_t pg, int32_t np, std::vector<int32_t>& seg_len) {
+        if (dev && np > 1) {
+            dev->count(pg, np, seg_len);
+            return;
+        }
         seg_len.assign(static_cast<size_t>(np) * n_out, 0);
         if (np == 1) {  // one panel: the segments are the outputs
             for (int32_t o = 0; o < n_out; ++o)
@@ -301,7 +305,21 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
     if (L.n_entries >= (int64_t(1) << 32)) throw std::length_error("too many entries for 32-bit units");
 
     tp[2] = clk();
+    if (dev) {  // the device fills the entries: per segment, padded position - source position
+        L.seg_delta.assign(seg_len.size(), 0);
+        parallel_for_outputs(start, out_begin, n_out, [&](int64_t ob, int64_t oe) {
+            for (int64_t o = ob; o < oe; ++o) {
+                int64_t src = start[out_begin + o];
+                for (int32_t p = 0; p < np; ++p) {
+                    const size_t s = static_cast<size_t>(p) * n_out + o;
+                    L.seg_delta[s] = seg_off[s] - src;
+                    src += seg_len[s];
+                }
+            }
+        });
+    }
     // ---- 3. fill entries (padding of each segment written by its owner thread) -----------------
+    if (!dev) {
     if (L.idx16) L.idx16v.alloc(L.n_entries);
     else L.idx32v.alloc(L.n_entries);
     L.val.alloc(L.n_entries);
@@ -344,6 +362,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
             if (cur_p >= 0) pad(w, wend);
         }
     });
+    }  // !dev
 
     tp[3] = clk();
     // ---- 4. units ----------------------------------------------------------------------------
@@ -535,7 +554,7 @@ SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const f
 
     tp[5] = clk();
     // ---- 6. sub-panel split points of the residual pass (entries are ascending within a unit) ---
-    if (L.rmw_sub > 1) {
+    if (L.rmw_sub > 1 && !dev) {
         const int S = L.rmw_sub;
         L.usplit.assign(static_cast<size_t>(nu) * (S + 1), 0);
         parallel_for(nu, [&](int64_t b, int64_t e) {
@@ -581,11 +600,8 @@ void for_each_entry(const SweepLayout& L, const std::function<void(int32_t, int6
 
 AlsLayout build_als_layout(const int64_t* start, const int32_t* idx, const float* val,
                            int32_t out_begin, int32_t out_end, const int32_t* gmap, int chunk) {
-    AlsLayout L;
-    const int32_t n_out = out_end - out_begin;
-    L.n_out = n_out;
+    AlsLayout L = build_als_structure(start, out_begin, out_end, chunk);
     const int64_t base = start[out_begin];
-    L.n_entries = start[out_end] - base;
     L.idx.resize(L.n_entries);
     L.val.resize(L.n_entries);
     parallel_for(L.n_entries, [&](int64_t b, int64_t e) {
@@ -594,6 +610,15 @@ AlsLayout build_als_layout(const int64_t* start, const int32_t* idx, const float
             L.val[x] = val[base + x];
         }
     });
+    return L;
+}
+
+AlsLayout build_als_structure(const int64_t* start, int32_t out_begin, int32_t out_end, int chunk) {
+    AlsLayout L;
+    const int32_t n_out = out_end - out_begin;
+    L.n_out = n_out;
+    const int64_t base = start[out_begin];
+    L.n_entries = start[out_end] - base;
     std::vector<int32_t> cnt(n_out, 0);
     for (int32_t o = 0; o < n_out; ++o) {
         const int64_t b = start[out_begin + o] - base, e = start[out_begin + o + 1] - base;

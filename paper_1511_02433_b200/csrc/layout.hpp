@@ -168,6 +168,7 @@ struct SweepLayout {
     bool flat = false;
     std::vector<FlatChunk> chunks;    // pieces' chunks: Piece::pad[0..1] = chunk range
     std::vector<uint32_t> tailbits;   // (n_entries / 4) bits + 24 words of slack
+    std::vector<int64_t> seg_delta;   // device-built sides: per segment p * n_out + o (see build_sweep_layout)
 };
 
 // Shared-memory floats one staged vector of `width` occupies (sentinel slot, 16-byte rounded).
@@ -179,10 +180,19 @@ inline int64_t stage_stride_floats(int64_t width) { return ((width + 1) + 3) & ~
 // number of gather vectors the fused promote sweep stages (2 on the CSR side, 3 on the CSC side);
 // panels are as wide as ONE staged vector allows (the 14 plain sweeps of a step stage one), and the
 // promote is split when its vectors do not fit (PMF_PANEL_ARRAYS=n sizes panels for n vectors).
+//
+// Device-resident sides (pmf_ctx_create_from_triplets): with `dev` set, idx / val are not read (they
+// may be null) -- the per-(panel, output) segment lengths come from dev->count (computed on the device
+// from its CSR / CSC), steps that touch entries are skipped (idx16v / idx32v / val stay empty, usplit
+// is left to the device), and seg_delta keeps, per segment (p, o), padded position - source position
+// of its entries, for the device fill (layout_fill_device).
+struct SegCounter {
+    std::function<void(int32_t pg, int32_t np, std::vector<int32_t>& seg_len)> count;
+};
 SweepLayout build_sweep_layout(const int64_t* start, const int32_t* idx, const float* val,
                                int32_t out_begin, int32_t out_end, const int32_t* gmap,
                                int32_t gat_extent, int stage_arrays, int smem_budget_bytes,
-                               int ctas, bool allow_idx16 = true);
+                               int ctas, bool allow_idx16 = true, const SegCounter* dev = nullptr);
 
 // Positions of the original entries of output o (in reference order) inside the padded layout:
 // calls fn(o, real_pos_in_output, padded_pos) for every real entry.
@@ -203,6 +213,8 @@ struct AlsLayout {
 
 AlsLayout build_als_layout(const int64_t* start, const int32_t* idx, const float* val,
                            int32_t out_begin, int32_t out_end, const int32_t* gmap, int chunk);
+// The same without idx / val (they stay empty): units, slots and empty outputs from `start` alone.
+AlsLayout build_als_structure(const int64_t* start, int32_t out_begin, int32_t out_end, int chunk);
 
 // runtime.hpp:91-136 partition_balanced (bounds p+1); returns false on invalid input.
 bool partition_balanced(const int64_t* costs, int32_t count, int p, int32_t* bounds);

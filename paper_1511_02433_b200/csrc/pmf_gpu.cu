@@ -483,7 +483,15 @@ void ensure_device() {
     (void)hooks;
 }
 
-DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
+// A side kept in HBM after the device ingest (contexts built from triplets): CSR / CSC arrays.
+struct DevSide {
+    const int64_t* start = nullptr;
+    const int32_t* idx = nullptr;
+    const float* val = nullptr;
+    int64_t nnz = 0;
+};
+
+DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy, const DevSide* src = nullptr) {
     DevSweep D;
     D.n_out = L.n_out;
     D.gat_extent = L.gat_extent;
@@ -513,11 +521,24 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     D.ctas = L.ctas;
     D.n_slots = L.n_slots;
     // slack: the flat kernels load whole 16-entry lane ranges past a layout's last vector (masked)
-    if (L.idx16) D.idx = c.mem.upload(L.idx16v, c.stream, &c.h2d, kStreamSlack);
-    else D.idx = c.mem.upload(L.idx32v, c.stream, &c.h2d, kStreamSlack);
+    DevMem tmp;
+    float* A = nullptr;
+    if (src) {  // the padded streams filled on the device from its CSR / CSC (layout_device.cu)
+        if (L.idx16) D.idx = c.mem.alloc<uint16_t>(static_cast<size_t>(L.n_entries) + kStreamSlack, false);
+        else D.idx = c.mem.alloc<int32_t>(static_cast<size_t>(L.n_entries) + kStreamSlack, false);
+        A = c.mem.alloc<float>(static_cast<size_t>(L.n_entries), false);
+        const int64_t* delta = tmp.upload(L.seg_delta, c.stream, &c.h2d);
+        layout_fill_device(src->start, src->idx, src->val, L.n_out, src->nnz, L.panel_size, L.n_panels, delta, L.idx16,
+                           L.sentinel, L.n_entries, D.idx, A, c.stream);
+        CUDA_TRY(cudaGetLastError());
+    } else {
+        if (L.idx16) D.idx = c.mem.upload(L.idx16v, c.stream, &c.h2d, kStreamSlack);
+        else D.idx = c.mem.upload(L.idx32v, c.stream, &c.h2d, kStreamSlack);
+        A = c.mem.upload(L.val, c.stream, &c.h2d);
+    }
     D.R = c.mem.alloc<float>(L.n_entries + kStreamSlack, false);
-    float* A = c.mem.upload(L.val, c.stream, &c.h2d);
-    CUDA_TRY(cudaMemcpyAsync(D.R, A, L.val.size() * sizeof(float), cudaMemcpyDeviceToDevice, c.stream));
+    CUDA_TRY(cudaMemcpyAsync(D.R, A, static_cast<size_t>(L.n_entries) * sizeof(float), cudaMemcpyDeviceToDevice,
+                             c.stream));
     *A_copy = A;
     D.units = c.mem.upload(L.units, c.stream, &c.h2d);
     D.unit_panel = c.mem.upload(L.unit_panel, c.stream, &c.h2d);
@@ -541,6 +562,15 @@ DevSweep upload_sweep(Ctx& c, SweepLayout& L, float** A_copy) {
     D.rmw_sub = L.rmw_sub;
     D.sub_width = L.sub_width;
     if (!L.usplit.empty()) D.usplit = c.mem.upload(L.usplit, c.stream, &c.h2d);
+    if (src && L.rmw_sub > 1) {  // sub-panel split points from the device-filled indices
+        if (!L.idx16) throw PmfError(PMF_RUNTIME_ERROR, "split promote needs 16-bit indices");
+        const int S = L.rmw_sub;
+        D.usplit = c.mem.alloc<uint16_t>(L.units.size() * static_cast<size_t>(S + 1), false);
+        const int32_t* real = tmp.upload(L.unit_real, c.stream, &c.h2d);
+        usplit_device(D.units, real, static_cast<int64_t>(L.units.size()), static_cast<const uint16_t*>(D.idx), S,
+                      L.sub_width, D.usplit, c.stream);
+        CUDA_TRY(cudaGetLastError());
+    }
     CUDA_TRY(cudaStreamSynchronize(c.stream));
     // keep only the metadata needed for residual readback
     L.idx16v.reset();
@@ -567,6 +597,77 @@ void dist_plan(const int64_t* row_start, int32_t m, const int64_t* col_start, in
     }
     *Bm = world == 1 ? m : bm;
     *Bn = world == 1 ? n : bn;
+}
+
+// Upload + device build of the CSR / CSC (sparse.hpp:73-149, csrc/ingest.cu) with the host builder's
+// validation errors: the first offending triplet in input order, then the first duplicate in row
+// order.  The four nnz-sized arrays come from `keep`, the rest from `tmp`.
+struct DevCsr {
+    int64_t* rs = nullptr;
+    int64_t* cs = nullptr;
+    int32_t* co = nullptr;
+    int32_t* ro = nullptr;
+    float* vr = nullptr;
+    float* vc = nullptr;
+};
+
+void check_triplet_args(const pmf_triplet* t, int64_t nnz, int32_t m, int32_t n) {
+    if (m < 0 || n < 0) invalid("matrix dimensions must be non-negative");
+    if (nnz < 0 || (nnz > 0 && !t)) invalid("from_triplets: null buffers");
+    if (nnz >= (int64_t(1) << 31)) invalid("from_triplets_gpu: more than 2^31 - 1 triplets");
+}
+
+DevCsr device_ingest(const pmf_triplet* t, int64_t nnz, int32_t m, int32_t n, cudaStream_t s, DevMem& keep,
+                     DevMem& tmp, double* t_up, double* t_build) {
+    const double t0 = now_s();
+    const size_t N = static_cast<size_t>(nnz > 0 ? nnz : 1);
+    DevCsr d;
+    auto* dt = tmp.alloc<DevTriplet>(N, false);
+    if (nnz > 0) staged_h2d(dt, t, sizeof(DevTriplet) * static_cast<size_t>(nnz), s);
+    d.rs = tmp.alloc<int64_t>(static_cast<size_t>(m) + 1, false);
+    d.cs = tmp.alloc<int64_t>(static_cast<size_t>(n) + 1, false);
+    d.co = keep.alloc<int32_t>(N, false);
+    d.ro = keep.alloc<int32_t>(N, false);
+    d.vr = keep.alloc<float>(N, false);
+    d.vc = keep.alloc<float>(N, false);
+    void* scratch = tmp.alloc<char>(ingest_scratch_bytes(nnz), false);
+    CUDA_TRY(cudaStreamSynchronize(s));
+    const double t1 = now_s();
+    int64_t bad = -1, dup = -1;
+    CUDA_TRY(ingest_build(dt, nnz, m, n, scratch, d.rs, d.co, d.vr, d.cs, d.ro, d.vc, &bad, &dup, s));
+    CUDA_TRY(cudaStreamSynchronize(s));
+    if (t_up) *t_up = t1 - t0;
+    if (t_build) *t_build = now_s() - t1;
+    if (bad >= 0) {  // the first offending triplet in input order decides (sparse.hpp:82-92)
+        const pmf_triplet& b = t[bad];
+        if (b.user < 0 || b.user >= m)
+            throw PmfError(PMF_OUT_OF_RANGE, "user index " + std::to_string(b.user) + " out of range for m=" +
+                                                 std::to_string(m));
+        if (b.item < 0 || b.item >= n)
+            throw PmfError(PMF_OUT_OF_RANGE, "item index " + std::to_string(b.item) + " out of range for n=" +
+                                                 std::to_string(n));
+        invalid("non-finite rating at user " + std::to_string(b.user));
+    }
+    if (dup >= 0) {  // sparse.hpp:127-132: first duplicate in row order
+        int32_t item = 0;
+        std::vector<int64_t> row_start(static_cast<size_t>(m) + 1);
+        CUDA_TRY(cudaMemcpyAsync(&item, d.co + dup, sizeof(item), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaMemcpyAsync(row_start.data(), d.rs, sizeof(int64_t) * row_start.size(), cudaMemcpyDeviceToHost, s));
+        CUDA_TRY(cudaStreamSynchronize(s));
+        const int64_t i = std::upper_bound(row_start.begin(), row_start.end(), dup) - row_start.begin() - 1;
+        invalid("duplicate rating for user " + std::to_string(i) + ", item " + std::to_string(item));
+    }
+    return d;
+}
+
+void set_kernel_attributes() {
+    static bool attrs_set = false;
+    if (!attrs_set) {
+        sweep_set_attributes(kSmemMax + 1024);
+        flat_set_attributes(kSmemMax + 1024);
+        als_set_attributes();
+        attrs_set = true;
+    }
 }
 
 std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, int world, const uint8_t* id) {
@@ -626,13 +727,7 @@ std::unique_ptr<Ctx> make_ctx(const pmf_matrix_view* a, int device, int rank, in
     c->local_nnz_csc = a->col_start[c->col_end] - a->col_start[c->col_begin];
     c->row_start_local.assign(a->row_start + c->row_begin, a->row_start + c->row_end + 1);
     c->col_start_local.assign(a->col_start + c->col_begin, a->col_start + c->col_end + 1);
-    static bool attrs_set = false;
-    if (!attrs_set) {
-        sweep_set_attributes(kSmemMax + 1024);
-        flat_set_attributes(kSmemMax + 1024);
-        als_set_attributes();
-        attrs_set = true;
-    }
+    set_kernel_attributes();
     const double t_upload = now_s();
     c->csr = upload_sweep(*c, c->hcsr, &c->A_csr);
     const double t_csr = now_s();
@@ -1001,6 +1096,93 @@ void build_als(Ctx& c, const pmf_matrix_view* a) {
     c.d_status = c.als_mem.alloc<int>(4);
     CUDA_TRY(cudaStreamSynchronize(c.stream));
     c.als_built = true;
+}
+
+// A context straight from triplets (world 1): the device ingest's CSR / CSC stay in HBM -- they are the
+// ALS streams, and the sweep layouts are filled from them on the device; the host receives only the
+// row / column offsets and the per-(panel, output) segment lengths, from which it builds the layouts'
+// structure (units, slots, CTA partition).  Bitwise the layouts of make_ctx on the same matrix.
+std::unique_ptr<Ctx> make_ctx_from_triplets(const pmf_triplet* t, int64_t nnz, int32_t m, int32_t n, int device) {
+    check_triplet_args(t, nnz, m, n);
+    ensure_device();
+    const double t0 = now_s();
+    auto c = std::make_unique<Ctx>();
+    if (device < 0) CUDA_TRY(cudaGetDevice(&device));
+    c->device = device;
+    CUDA_TRY(cudaSetDevice(device));
+    CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventCreateWithFlags(&c->ev_sent, cudaEventDisableTiming));
+    CUDA_TRY(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+    c->m = m;
+    c->n = n;
+    c->nnz = nnz;
+    DevMem tmp;
+    double tu = 0, tb = 0;
+    const DevCsr d = device_ingest(t, nnz, m, n, c->stream, c->als_mem, tmp, &tu, &tb);
+    c->h2d += static_cast<int64_t>(sizeof(pmf_triplet)) * nnz;
+    const double t_ingest = now_s();
+    c->row_start_local.resize(static_cast<size_t>(m) + 1);
+    c->col_start_local.resize(static_cast<size_t>(n) + 1);
+    CUDA_TRY(cudaMemcpyAsync(c->row_start_local.data(), d.rs, sizeof(int64_t) * c->row_start_local.size(),
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaMemcpyAsync(c->col_start_local.data(), d.cs, sizeof(int64_t) * c->col_start_local.size(),
+                             cudaMemcpyDeviceToHost, c->stream));
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->Bm = m;
+    c->Bn = n;
+    c->row_end = m;
+    c->col_end = n;
+    c->ext_m = m;
+    c->ext_n = n;
+    c->ldm = ((c->ext_m + 4 + 31) / 32) * 32;
+    c->ldn = ((c->ext_n + 4 + 31) / 32) * 32;
+    c->local_nnz_csr = c->local_nnz_csc = nnz;
+    DevMem segmem;
+    auto counter = [&](const int64_t* dstart, const int32_t* didx, int32_t n_out) {
+        return SegCounter{[&c, &segmem, dstart, didx, n_out](int32_t pg, int32_t np, std::vector<int32_t>& seg_len) {
+            const size_t total = static_cast<size_t>(np) * n_out;
+            int32_t* buf = segmem.alloc<int32_t>(total, false);
+            seg_count_device(dstart, didx, n_out, pg, np, buf, c->stream);
+            CUDA_TRY(cudaGetLastError());
+            seg_len.resize(total);
+            staged_d2h(seg_len.data(), buf, total * sizeof(int32_t), c->stream);
+        }};
+    };
+    const SegCounter ccsr = counter(d.rs, d.co, m), ccsc = counter(d.cs, d.ro, n);
+    c->hcsr = build_sweep_layout(c->row_start_local.data(), nullptr, nullptr, 0, m, nullptr, c->ext_n, 2,
+                                 smem_budget(), c->sm_count, true, &ccsr);
+    c->hcsc = build_sweep_layout(c->col_start_local.data(), nullptr, nullptr, 0, n, nullptr, c->ext_m, 3,
+                                 smem_budget(), c->sm_count, true, &ccsc);
+    const double t_layout = now_s();
+    set_kernel_attributes();
+    const DevSide scsr{d.rs, d.co, d.vr, nnz}, scsc{d.cs, d.ro, d.vc, nnz};
+    c->csr = upload_sweep(*c, c->hcsr, &c->A_csr, &scsr);
+    c->csc = upload_sweep(*c, c->hcsc, &c->A_csc, &scsc);
+    c->unit_loss = c->eval_mem.alloc<double>(std::max(c->csr.n_units, 1));
+    c->red_scratch = c->eval_mem.alloc<double>(4096);
+    c->red_out = c->eval_mem.alloc<double>(8);
+    // ALS streams: the device CSR / CSC themselves (world 1: identity index space)
+    const int chunk = als_chunk(c->nnz, c->sm_count);
+    AlsLayout lc = build_als_structure(c->row_start_local.data(), 0, m, chunk);
+    AlsLayout lr = build_als_structure(c->col_start_local.data(), 0, n, chunk);
+    c->als_csr = upload_als(*c, lc, 0);
+    c->als_csc = upload_als(*c, lr, 0);
+    c->als_csr.idx = d.co;
+    c->als_csr.val = d.vr;
+    c->als_csc.idx = d.ro;
+    c->als_csc.val = d.vc;
+    c->d_counter = c->als_mem.alloc<int>(4);
+    c->d_status = c->als_mem.alloc<int>(4);
+    c->als_built = true;
+    CUDA_TRY(cudaStreamSynchronize(c->stream));
+    c->setup_seconds = now_s() - t0;
+    if (std::getenv("PMF_VERBOSE"))
+        std::fprintf(stderr,
+                     "[pmf] ctx from triplets %.3f s: upload %.3f, device CSR/CSC %.3f, offsets %.3f, layout "
+                     "structure %.3f, device fill + uploads %.3f\n",
+                     c->setup_seconds, tu, tb, t_ingest - t0 - tu - tb, t_layout - t_ingest, now_s() - t_layout);
+    return c;
 }
 
 // A device group of `world` ranks in this process: rank r owns CSR row block r and CSC column block r
@@ -1454,6 +1636,15 @@ pmf_status pmf_ctx_create(const pmf_matrix_view* a, int32_t device, pmf_ctx** ou
     });
 }
 
+pmf_status pmf_ctx_create_from_triplets(const pmf_triplet* triplets, int64_t nnz, int32_t m, int32_t n,
+                                        int32_t device, pmf_ctx** out) {
+    return guard([&] {
+        if (!out) invalid("out is null");
+        auto c = make_ctx_from_triplets(triplets, nnz, m, n, device);
+        *out = reinterpret_cast<pmf_ctx*>(c.release());
+    });
+}
+
 pmf_status pmf_ctx_create_dist(const pmf_matrix_view* a, int32_t device, int32_t rank, int32_t world,
                                const uint8_t* id, pmf_ctx** out) {
     return guard([&] {
@@ -1616,12 +1807,10 @@ pmf_status pmf_matrix_from_triplets_gpu(const pmf_triplet* t, int64_t nnz, int32
                                         int64_t* row_start, int32_t* col_of, float* val_row, int64_t* col_start,
                                         int32_t* row_of, float* val_col) {
     return guard([&] {
-        if (m < 0 || n < 0) invalid("matrix dimensions must be non-negative");
-        if (nnz < 0 || (nnz > 0 && (!t || !col_of || !val_row || !row_of || !val_col)) || !row_start || !col_start)
-            invalid("from_triplets: null buffers");
-        if (nnz >= (int64_t(1) << 31)) invalid("from_triplets_gpu: more than 2^31 - 1 triplets");
+        check_triplet_args(t, nnz, m, n);
+        if (nnz > 0 && (!col_of || !val_row || !row_of || !val_col)) invalid("from_triplets: null buffers");
+        if (!row_start || !col_start) invalid("from_triplets: null buffers");
         ensure_device();
-        const double t0 = now_s();
         cudaStream_t s = nullptr;
         CUDA_TRY(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
         struct StreamGuard {
@@ -1629,52 +1818,20 @@ pmf_status pmf_matrix_from_triplets_gpu(const pmf_triplet* t, int64_t nnz, int32
             ~StreamGuard() { cudaStreamDestroy(s); }
         } sg{s};
         DevMem mem;
-        const size_t N = static_cast<size_t>(nnz > 0 ? nnz : 1);
-        auto* dt = mem.alloc<DevTriplet>(N, false);
-        if (nnz > 0) staged_h2d(dt, t, sizeof(DevTriplet) * static_cast<size_t>(nnz), s);
-        auto* rs = mem.alloc<int64_t>(static_cast<size_t>(m) + 1, false);
-        auto* cs = mem.alloc<int64_t>(static_cast<size_t>(n) + 1, false);
-        auto* co = mem.alloc<int32_t>(N, false);
-        auto* ro = mem.alloc<int32_t>(N, false);
-        auto* vr = mem.alloc<float>(N, false);
-        auto* vc = mem.alloc<float>(N, false);
-        void* scratch = mem.alloc<char>(ingest_scratch_bytes(nnz), false);
-        CUDA_TRY(cudaStreamSynchronize(s));
-        const double t1 = now_s();
-        int64_t bad = -1, dup = -1;
-        CUDA_TRY(ingest_build(dt, nnz, m, n, scratch, rs, co, vr, cs, ro, vc, &bad, &dup, s));
-        CUDA_TRY(cudaStreamSynchronize(s));
+        double tu = 0, tb = 0;
+        const DevCsr d = device_ingest(t, nnz, m, n, s, mem, mem, &tu, &tb);
         const double t2 = now_s();
-        if (bad >= 0) {  // the first offending triplet in input order decides (sparse.hpp:82-92)
-            const pmf_triplet& b = t[bad];
-            if (b.user < 0 || b.user >= m)
-                throw PmfError(PMF_OUT_OF_RANGE, "user index " + std::to_string(b.user) + " out of range for m=" +
-                                                     std::to_string(m));
-            if (b.item < 0 || b.item >= n)
-                throw PmfError(PMF_OUT_OF_RANGE, "item index " + std::to_string(b.item) + " out of range for n=" +
-                                                     std::to_string(n));
-            invalid("non-finite rating at user " + std::to_string(b.user));
-        }
-        if (dup >= 0) {  // sparse.hpp:127-132: first duplicate in row order
-            int32_t item = 0;
-            CUDA_TRY(cudaMemcpyAsync(&item, co + dup, sizeof(item), cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaMemcpyAsync(row_start, rs, sizeof(int64_t) * (static_cast<size_t>(m) + 1),
-                                     cudaMemcpyDeviceToHost, s));
-            CUDA_TRY(cudaStreamSynchronize(s));
-            const int64_t i = std::upper_bound(row_start, row_start + m + 1, dup) - row_start - 1;
-            invalid("duplicate rating for user " + std::to_string(i) + ", item " + std::to_string(item));
-        }
-        staged_d2h(row_start, rs, sizeof(int64_t) * (static_cast<size_t>(m) + 1), s);
-        staged_d2h(col_start, cs, sizeof(int64_t) * (static_cast<size_t>(n) + 1), s);
+        staged_d2h(row_start, d.rs, sizeof(int64_t) * (static_cast<size_t>(m) + 1), s);
+        staged_d2h(col_start, d.cs, sizeof(int64_t) * (static_cast<size_t>(n) + 1), s);
         if (nnz > 0) {
-            staged_d2h(col_of, co, sizeof(int32_t) * static_cast<size_t>(nnz), s);
-            staged_d2h(val_row, vr, sizeof(float) * static_cast<size_t>(nnz), s);
-            staged_d2h(row_of, ro, sizeof(int32_t) * static_cast<size_t>(nnz), s);
-            staged_d2h(val_col, vc, sizeof(float) * static_cast<size_t>(nnz), s);
+            staged_d2h(col_of, d.co, sizeof(int32_t) * static_cast<size_t>(nnz), s);
+            staged_d2h(val_row, d.vr, sizeof(float) * static_cast<size_t>(nnz), s);
+            staged_d2h(row_of, d.ro, sizeof(int32_t) * static_cast<size_t>(nnz), s);
+            staged_d2h(val_col, d.vc, sizeof(float) * static_cast<size_t>(nnz), s);
         }
         if (std::getenv("PMF_VERBOSE"))
-            std::fprintf(stderr, "[pmf] from_triplets_gpu: alloc + upload %.3f s, build %.3f, download %.3f\n", t1 - t0,
-                         t2 - t1, now_s() - t2);
+            std::fprintf(stderr, "[pmf] from_triplets_gpu: alloc + upload %.3f s, build %.3f, download %.3f\n", tu, tb,
+                         now_s() - t2);
     });
 }
 
