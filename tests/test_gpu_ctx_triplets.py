@@ -106,3 +106,23 @@ def test_errors_match_host_builder(pmf):
         with pytest.raises(Exception) as ed:
             pmf.Context.from_triplets(t, 3, 3)
         assert type(eh.value) is type(ed.value) and str(eh.value) == str(ed.value)
+
+
+@pytest.mark.slow
+def test_netflix_shape_bitwise(pmf):
+    """BASELINE configs[2] bytes (bench.make_data): one CCD++ outer iteration (k=40, T=15) and one ALS
+    iteration on a context from triplets and on one from the host matrix -- bitwise the same."""
+    import bench
+    train, probe = bench.make_data("netflix-ccdpp")
+    host, dev = _pair(pmf, train, 480189, 17770)
+    for c in (host, dev):
+        c.set_probe(probe)
+        c.ccdpp_begin(pmf.CcdConfig(k=40, lam=0.05, outer_iters=1, inner_iters=15, seed=1))
+        c.ccdpp_iterate(1)
+    _same(host, dev)
+    for c in (host, dev):
+        c.als_begin(pmf.AlsConfig(k=40, lam=0.05, outer_iters=1, seed=1))
+        c.als_iterate(1)
+    _same(host, dev)
+    host.close()
+    dev.close()
