@@ -72,10 +72,13 @@ int launch_finalize(const DevSweep& L, const SweepOperands& op, cudaStream_t str
 int launch_flat(const DevSweep& L, SweepMode mode, bool csr_side, const SweepOperands& op, cudaStream_t stream);
 void flat_set_attributes(size_t max_smem);
 // A whole CCD++ outer iteration for small single-panel layouts in one cluster kernel (small_kernels.cu).
-bool small_ccdpp_eligible(const DevSweep& csr, const DevSweep& csc, int64_t nnz);
-cudaError_t launch_small_ccdpp(const DevSweep& csr, const DevSweep& csc, float* W, float* H, float* ub, float* vb,
-                               int64_t ldm, int64_t ldn, int32_t m, int32_t n, int k, int inner, float lambda,
-                               cudaStream_t s);
+// Eligible: single-panel 16-bit layouts without partial slots whose per-CTA residual runs and the factor
+// columns fit one CTA's shared memory (MovieLens-100K: 86 KB).
+bool small_ccdpp_eligible(const DevSweep& csr, const DevSweep& csc, const SweepLayout& hcsr, const SweepLayout& hcsc,
+                          int32_t m, int32_t n);
+cudaError_t launch_small_ccdpp(const DevSweep& csr, const DevSweep& csc, const SweepLayout& hcsr,
+                               const SweepLayout& hcsc, float* W, float* H, float* ub, float* vb, int64_t ldm,
+                               int64_t ldn, int32_t m, int32_t n, int k, int inner, float lambda, cudaStream_t s);
 void sweep_set_attributes(size_t max_smem);
 
 // dst[i * k + t] = src[t * ld + i] for i < count (column-major k x ld factor -> row-major).

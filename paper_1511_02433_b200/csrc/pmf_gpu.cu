@@ -1019,18 +1019,18 @@ void ccd_iterate(Ctx& c, int n_outer, double* secs) {
         CUDA_TRY(cudaGraphInstantiate(&c.graph_exec, c.graph, 0));
         c.launches_per_iter = launched;
     }
-    // small matrices (one panel, no partial slots, <= 256K ratings): the whole iteration as one cluster
-    // kernel (small_kernels.cu) instead of 2 T k graph nodes
+    // small matrices (one panel, no partial slots, residual runs fit shared memory): the whole iteration
+    // as one cluster kernel (small_kernels.cu) instead of 2 T k graph nodes
     const bool small = cs.size() == 1 && !c.profiling && !small_disabled() &&
-                       small_ccdpp_eligible(c.csr, c.csc, c.nnz);
+                       small_ccdpp_eligible(c.csr, c.csc, c.hcsr, c.hcsc, c.m, c.n);
     cudaEvent_t e0, e1;
     CUDA_TRY(cudaEventCreate(&e0));
     CUDA_TRY(cudaEventCreate(&e1));
     for (int it = 0; it < n_outer; ++it) {
         CUDA_TRY(cudaEventRecord(e0, c.stream));
         if (small) {
-            CUDA_TRY(launch_small_ccdpp(c.csr, c.csc, c.W, c.H, c.ubuf, c.vbuf, c.ldm, c.ldn, c.m, c.n, c.k, c.inner,
-                                        c.lambda, c.stream));
+            CUDA_TRY(launch_small_ccdpp(c.csr, c.csc, c.hcsr, c.hcsc, c.W, c.H, c.ubuf, c.vbuf, c.ldm, c.ldn, c.m, c.n,
+                                        c.k, c.inner, c.lambda, c.stream));
             c.launches_per_iter = 1;
         } else if (!graph) c.launches_per_iter = enqueue_ccd_iteration(cs);
         else CUDA_TRY(cudaGraphLaunch(c.graph_exec, c.stream));
