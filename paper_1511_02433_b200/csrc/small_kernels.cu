@@ -14,7 +14,7 @@
 // H[t], H[t-1].  A unit's result is stored into all 16 CTAs' copy of u (or v) over distributed shared
 // memory (st.shared::cluster, one lane per CTA), so after the barrier every gather is a local
 // shared-memory read.  Per entry the arithmetic is the graph path's (products rounded before the
-// subtract / add, no FMA in the residual update, FMA sums; a warp per unit, 4-entry vectors per lane,
+// subtract / add, no FMA in the residual update, FMA sums; 8 lanes per unit, 4-entry vectors per lane,
 // xor-shuffle sums), so both residual copies stay bitwise equal; u, v agree with the graph path to
 // FP32 rounding (the graph path sums a unit's entries in a different fixed order).
 #include <cuda_runtime.h>
@@ -31,6 +31,12 @@ namespace {
 constexpr int kSmallThreads = 1024;
 constexpr int kSmallCtas = 16;
 constexpr int kSmallSmemMax = 200 * 1024;
+// lanes per unit (4 units per warp at once): ML-100K 0.83 ms per iteration with 8, 1.11 with 4, 1.01 with
+// 16, 1.51 with 32 (scripts/small_timing.py; the sweeps are issue-bound, shorter reductions win)
+#ifndef PMF_SMALL_G
+#define PMF_SMALL_G 8
+#endif
+constexpr int kSmallG = PMF_SMALL_G;
 
 __device__ __forceinline__ void cluster_sync_all() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;" ::: "memory");
@@ -57,26 +63,27 @@ struct SmallSide {
     int32_t elen[kSmallCtas];
 };
 
-// One sweep over the CTA's units of a side, a warp per unit (4-entry vectors per lane); Rs / Is: the
+// One sweep over the CTA's units of a side, G lanes per unit (4-entry vectors per lane); Rs / Is: the
 // CTA's resident residual / indices (entry e at e - ebase).  PROMOTE: the first sweep of a step,
 // R <- (R - oa_o ga_g) then + w h if w != 0 (CSR: w = ob_o, h = gb_g; CSC: w = gb_g, h = ob_o).
 // The result of output o goes to out[o] in every CTA of the cluster.
-template <bool PROMOTE, bool CSR>
+template <bool PROMOTE, bool CSR, int G>
 __device__ __forceinline__ void small_sweep(const SmallSide& S, int c, const Unit* Us, float* Rs, const uint16_t* Is,
                                             const float* ga, const float* gb, const float* gn, const float* oa,
                                             const float* ob, float* out, float lambda) {
+    constexpr int PER_WARP = 32 / G;  // units a warp works on together (a group of G lanes each)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int l = lane % G, grp = lane / G;
     const int nu = S.u0[c + 1] - S.u0[c];
     const int64_t ebase = S.e0[c];
-    const int ng = (nu + 31) / 32;  // uniform trip count per warp (the shuffles below are warp-wide)
-    for (int it = 0; it < ng; ++it) {
-        const int u = warp + 32 * it;
+    for (int u0 = warp * PER_WARP; u0 < nu; u0 += 32 * PER_WARP) {  // warp-uniform trip count
+        const int u = u0 + grp;
         const bool live = u < nu;
         const Unit U = live ? Us[u] : Unit{0u, 0, 0, -1};
         const float a_o = PROMOTE && live ? oa[U.o] : 0.f;
         const float b_o = PROMOTE && live ? ob[U.o] : 0.f;
         float num = 0.f, den = 0.f;
-        for (int v = lane; 4 * v < U.len; v += 32) {
+        for (int v = l; 4 * v < U.len; v += G) {
             const int64_t e = static_cast<int64_t>(U.e0) + 4 * v - ebase;
             float4 r4 = *reinterpret_cast<const float4*>(Rs + e);
             const uint2 ix = *reinterpret_cast<const uint2*>(Is + e);
@@ -103,13 +110,14 @@ __device__ __forceinline__ void small_sweep(const SmallSide& S, int c, const Uni
             if (PROMOTE) *reinterpret_cast<float4*>(Rs + e) = make_float4(rv[0], rv[1], rv[2], rv[3]);
         }
 #pragma unroll
-        for (int off = 16; off > 0; off >>= 1) {
+        for (int off = G / 2; off > 0; off >>= 1) {
             num += __shfl_xor_sync(0xffffffffu, num, off);
             den += __shfl_xor_sync(0xffffffffu, den, off);
         }
-        if (live && lane < kSmallCtas) {
+        if (live) {
             const float dt = __fadd_rn(lambda, den);
-            dsmem_st(out + U.o, lane, dt == 0.f ? 0.f : __fdiv_rn(num, dt));
+            const float z = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+            for (int r = l; r < kSmallCtas; r += G) dsmem_st(out + U.o, r, z);
         }
     }
 }
@@ -176,12 +184,12 @@ small_ccdpp_kernel(const __grid_constant__ SmallSide csr, const __grid_constant_
         __syncthreads();
         for (int s = 0; s < inner; ++s) {
             // u-sweep over CSR (gathered: v' = H[tp], h = H[t], v; per output: u' = W[tp], w = W[t])
-            if (s == 0) small_sweep<true, true>(csr, c, Ur, Rr, Ir, shp, sht, sht, swp, swt, su, lambda);
-            else small_sweep<false, true>(csr, c, Ur, Rr, Ir, nullptr, nullptr, sv, nullptr, nullptr, su, lambda);
+            if (s == 0) small_sweep<true, true, kSmallG>(csr, c, Ur, Rr, Ir, shp, sht, sht, swp, swt, su, lambda);
+            else small_sweep<false, true, kSmallG>(csr, c, Ur, Rr, Ir, nullptr, nullptr, sv, nullptr, nullptr, su, lambda);
             cluster_sync_all();
             // v-sweep over CSC (gathered: u' = W[tp], w = W[t], u; per output: v' = H[tp], h = H[t])
-            if (s == 0) small_sweep<true, false>(csc, c, Uc, Rc, Ic, swp, swt, su, shp, sht, sv, lambda);
-            else small_sweep<false, false>(csc, c, Uc, Rc, Ic, nullptr, nullptr, su, nullptr, nullptr, sv, lambda);
+            if (s == 0) small_sweep<true, false, kSmallG>(csc, c, Uc, Rc, Ic, swp, swt, su, shp, sht, sv, lambda);
+            else small_sweep<false, false, kSmallG>(csc, c, Uc, Rc, Ic, nullptr, nullptr, su, nullptr, nullptr, sv, lambda);
             cluster_sync_all();
         }
         // writeback of the column pair (ccd.hpp:209, :226), a slice per CTA; the residual part is deferred
