@@ -180,12 +180,16 @@ ccd_cols_kernel(const int64_t* __restrict__ col_start, const int32_t* __restrict
     }
 }
 
-// H sweep, longest columns first: CTAs of kColThreadsL claim columns from a counter over col_order (LPT;
+// H sweep, longest columns first: CTAs of kColThreadsL threads claim columns from a counter over col_order (LPT;
 // the popular columns hold up to ~5 % of the entries each), and gather w_it from the column-major copy
 // WT (k x m), so that the dense row ranges of long columns read coalesced.  One pass per coordinate t:
 // the pass of t applies the residual shift of t - 1 (R -= (z - h_j,t-1) w_i,t-1, the reference's
 // ccd_apply_s arithmetic, deferred) and accumulates the sums of t; a last pass applies the shift of k - 1.
-constexpr int kColThreadsL = 1024;
+// threads per column CTA (2 CTAs per SM): Netflix k = 40 epoch 37.3 ms with 512, 39.0 with 256, 40.1 with 1024
+#ifndef PMF_CCDW_COL_THREADS
+#define PMF_CCDW_COL_THREADS 512
+#endif
+constexpr int kColThreadsL = PMF_CCDW_COL_THREADS;
 __global__ void __launch_bounds__(kColThreadsL)
 ccd_cols_lpt_kernel(const int64_t* __restrict__ col_start, const int32_t* __restrict__ row_of, float* __restrict__ R,
                     const float* __restrict__ WT, float* __restrict__ H, int32_t n, int32_t m, int k, float lambda,
@@ -249,8 +253,8 @@ ccd_cols_lpt_kernel(const int64_t* __restrict__ col_start, const int32_t* __rest
             }
             __syncthreads();
             if (warp == 0) {
-                num = s_num[lane];
-                den = s_den[lane];
+                num = lane < kColThreadsL / 32 ? s_num[lane] : 0.f;
+                den = lane < kColThreadsL / 32 ? s_den[lane] : 0.f;
                 warp_sum2(num, den);
                 if (lane == 0) {
                     const float dt = __fadd_rn(lambda, den);
@@ -328,7 +332,7 @@ int launch_ccd_epoch(const CcdWs& ws, float* W, float* H, int k, float lambda, c
     if (ws.n > 0 && ws.WT) {
         ccd_transpose_kernel<<<dim3((ws.m + 31) / 32, (k + 31) / 32), dim3(32, 8), 0, s>>>(W, ws.WT, ws.m, k);
         cudaMemsetAsync(ws.counter, 0, sizeof(int), s);
-        ccd_cols_lpt_kernel<<<148, kColThreadsL, 0, s>>>(ws.col_start, ws.row_of, ws.R_col, ws.WT, H, ws.n, ws.m, k,
+        ccd_cols_lpt_kernel<<<148 * (1024 / kColThreadsL), kColThreadsL, 0, s>>>(ws.col_start, ws.row_of, ws.R_col, ws.WT, H, ws.n, ws.m, k,
                                                          lambda, ws.col_order, ws.counter);
         launched += 2;
     } else if (ws.n > 0) {
