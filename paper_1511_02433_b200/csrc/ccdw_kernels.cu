@@ -18,6 +18,7 @@
 // sums over a row / column are warp / CTA trees (reduction order differs, as everywhere on the GPU).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 
 #include "device.hpp"
@@ -66,73 +67,102 @@ __device__ __forceinline__ void warp_sum2(float& a, float& b) {
 }
 
 // W sweep (ccd.hpp:113-116): a warp per row; for each t the z* of ccd_z_star (:56-68) and the
-// residual shift of ccd_apply_z (:73-80).  The row's residual sits in registers for rows <= 256.
-__global__ void ccd_rows_kernel(const int64_t* __restrict__ row_start, const int32_t* __restrict__ col_of,
-                                float* __restrict__ R, float* __restrict__ W, const float* __restrict__ H,
-                                int32_t m, int k, float lambda) {
+// residual shift of ccd_apply_z (:73-80).  Rows <= 256 entries keep their residual in registers and
+// take the gathered h of kRowChunk coordinates at once: one 4 kRowChunk-byte read of the row-major H
+// row per entry (a 32-byte sector serves kRowChunk coordinates instead of one), parked in the warp's
+// shared-memory slice (each lane only touches its own entries' values), and the row's w of the chunk
+// by one load; longer rows stream R and gather per coordinate.
+#ifndef PMF_CCDW_ROW_CHUNK
+#define PMF_CCDW_ROW_CHUNK 8
+#endif
+constexpr int kRowChunk = PMF_CCDW_ROW_CHUNK;
+constexpr int kRowThreads = 256;
+constexpr int kRowSmemFloats = (kRowThreads / 32) * kRowChunk * kRowCache * 32;
+__global__ void __launch_bounds__(kRowThreads, 3)
+ccd_rows_kernel(const int64_t* __restrict__ row_start, const int32_t* __restrict__ col_of,
+                float* __restrict__ R, float* __restrict__ W, const float* __restrict__ H,
+                int32_t m, int k, float lambda) {
+    extern __shared__ __align__(16) float rsm[];
     const int lane = threadIdx.x & 31;
+    float* hs = rsm + (threadIdx.x >> 5) * (kRowChunk * kRowCache * 32);  // [q][c][lane]
+    const bool vec = (k & 3) == 0 && (kRowChunk & 3) == 0;
     for (int64_t i = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < m;
          i += (static_cast<int64_t>(gridDim.x) * blockDim.x) >> 5) {
         const int64_t b = row_start[i], e = row_start[i + 1];
-        const bool cached = e - b <= 32 * kRowCache;
-        float r[kRowCache];
-        int32_t jj[kRowCache];
-        if (cached) {
+        if (e - b <= 32 * kRowCache) {
+            float r[kRowCache];
+            int32_t jj[kRowCache];
 #pragma unroll
             for (int c = 0; c < kRowCache; ++c) {
                 const int64_t p = b + lane + 32 * c;
                 r[c] = p < e ? R[p] : 0.f;
-                jj[c] = p < e ? col_of[p] : 0;
+                jj[c] = p < e ? col_of[p] : -1;
             }
-        }
-        // cached rows: the gathered h of coordinate t + 1 are loaded while t is reduced (its h only
-        // depends on the fixed H), so the L2 gathers are off the t-to-t dependency chain
-        float hn[kRowCache];
-        if (cached) {
-#pragma unroll
-            for (int c = 0; c < kRowCache; ++c) hn[c] = b + lane + 32 * c < e ? H[static_cast<int64_t>(jj[c]) * k] : 0.f;
-        }
-        for (int t = 0; t < k; ++t) {
-            const float wit = W[i * k + t];
-            float num = 0.f, den = 0.f;
-            float hc[kRowCache];
-            if (cached) {
+            for (int t0 = 0; t0 < k; t0 += kRowChunk) {
+                const int cc = min(kRowChunk, k - t0);
 #pragma unroll
                 for (int c = 0; c < kRowCache; ++c) {
-                    hc[c] = hn[c];
-                    const bool in = b + lane + 32 * c < e;
-                    if (t + 1 < k) hn[c] = in ? H[static_cast<int64_t>(jj[c]) * k + t + 1] : 0.f;
-                    if (in) {
-                        num = __fadd_rn(num, __fmul_rn(__fadd_rn(r[c], __fmul_rn(wit, hc[c])), hc[c]));
-                        den = __fadd_rn(den, __fmul_rn(hc[c], hc[c]));
+                    if (jj[c] < 0) continue;
+                    const float* src = H + static_cast<int64_t>(jj[c]) * k + t0;
+                    if (vec && cc == kRowChunk) {
+#pragma unroll
+                        for (int q = 0; q < kRowChunk; q += 4) {
+                            const float4 v = *reinterpret_cast<const float4*>(src + q);
+                            hs[((q + 0) * kRowCache + c) * 32 + lane] = v.x;
+                            hs[((q + 1) * kRowCache + c) * 32 + lane] = v.y;
+                            hs[((q + 2) * kRowCache + c) * 32 + lane] = v.z;
+                            hs[((q + 3) * kRowCache + c) * 32 + lane] = v.w;
+                        }
+                    } else {
+                        for (int q = 0; q < cc; ++q) hs[(q * kRowCache + c) * 32 + lane] = src[q];
                     }
                 }
-            } else {
-                for (int64_t p = b + lane; p < e; p += 32) {
-                    const float h = H[static_cast<int64_t>(col_of[p]) * k + t];
-                    num = __fadd_rn(num, __fmul_rn(__fadd_rn(R[p], __fmul_rn(wit, h)), h));
-                    den = __fadd_rn(den, __fmul_rn(h, h));
-                }
-            }
-            warp_sum2(num, den);
-            const float dt = __fadd_rn(lambda, den);
-            const float z = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
-            const float delta = __fsub_rn(z, wit);
-            if (cached) {
+                const float wl = lane < cc ? W[i * k + t0 + lane] : 0.f;
+                float zl = 0.f;
+                for (int tt = 0; tt < cc; ++tt) {
+                    const float wit = __shfl_sync(0xffffffffu, wl, tt);
+                    float num = 0.f, den = 0.f;
+                    float hc[kRowCache];
 #pragma unroll
-                for (int c = 0; c < kRowCache; ++c) r[c] = __fsub_rn(r[c], __fmul_rn(delta, hc[c]));
-            } else {
-                for (int64_t p = b + lane; p < e; p += 32)
-                    R[p] = __fsub_rn(R[p], __fmul_rn(delta, H[static_cast<int64_t>(col_of[p]) * k + t]));
+                    for (int c = 0; c < kRowCache; ++c) {
+                        hc[c] = jj[c] >= 0 ? hs[(tt * kRowCache + c) * 32 + lane] : 0.f;
+                        if (jj[c] >= 0) {
+                            num = __fadd_rn(num, __fmul_rn(__fadd_rn(r[c], __fmul_rn(wit, hc[c])), hc[c]));
+                            den = __fadd_rn(den, __fmul_rn(hc[c], hc[c]));
+                        }
+                    }
+                    warp_sum2(num, den);
+                    const float dt = __fadd_rn(lambda, den);
+                    const float z = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+                    const float delta = __fsub_rn(z, wit);
+#pragma unroll
+                    for (int c = 0; c < kRowCache; ++c) r[c] = __fsub_rn(r[c], __fmul_rn(delta, hc[c]));
+                    if (lane == tt) zl = z;
+                }
+                if (lane < cc) W[i * k + t0 + lane] = zl;
             }
-            if (lane == 0) W[i * k + t] = z;
-        }
-        if (cached) {
 #pragma unroll
             for (int c = 0; c < kRowCache; ++c) {
                 const int64_t p = b + lane + 32 * c;
                 if (p < e) R[p] = r[c];
             }
+            continue;
+        }
+        for (int t = 0; t < k; ++t) {
+            const float wit = W[i * k + t];
+            float num = 0.f, den = 0.f;
+            for (int64_t p = b + lane; p < e; p += 32) {
+                const float h = H[static_cast<int64_t>(col_of[p]) * k + t];
+                num = __fadd_rn(num, __fmul_rn(__fadd_rn(R[p], __fmul_rn(wit, h)), h));
+                den = __fadd_rn(den, __fmul_rn(h, h));
+            }
+            warp_sum2(num, den);
+            const float dt = __fadd_rn(lambda, den);
+            const float z = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+            const float delta = __fsub_rn(z, wit);
+            for (int64_t p = b + lane; p < e; p += 32)
+                R[p] = __fsub_rn(R[p], __fmul_rn(delta, H[static_cast<int64_t>(col_of[p]) * k + t]));
+            if (lane == 0) W[i * k + t] = z;
         }
     }
 }
@@ -190,14 +220,29 @@ ccd_cols_kernel(const int64_t* __restrict__ col_start, const int32_t* __restrict
 #define PMF_CCDW_COL_THREADS 512
 #endif
 constexpr int kColThreadsL = PMF_CCDW_COL_THREADS;
+#ifndef PMF_CCDW_COL_CACHE
+#define PMF_CCDW_COL_CACHE 16
+#endif
+// residual entries per thread of a cached column (columns <= 8K entries: ~46 % of Netflix's ratings) and
+// coordinates gathered per chunk: Netflix k = 40 epoch 25.4 ms with 16 / 4, 26.6 with 8 / 4, 28.7 with 16 / 2,
+// 32.0 without the cached path (scripts/ccdw_run.py)
+constexpr int kColCache = PMF_CCDW_COL_CACHE;
+#ifndef PMF_CCDW_COL_CHUNK
+#define PMF_CCDW_COL_CHUNK 4
+#endif
+constexpr int kColChunk = PMF_CCDW_COL_CHUNK;
+constexpr int kColSmemFloats = kColChunk * kColCache * kColThreadsL;
 __global__ void __launch_bounds__(kColThreadsL)
 ccd_cols_lpt_kernel(const int64_t* __restrict__ col_start, const int32_t* __restrict__ row_of, float* __restrict__ R,
-                    const float* __restrict__ WT, float* __restrict__ H, int32_t n, int32_t m, int k, float lambda,
-                    const int32_t* __restrict__ col_order, int* __restrict__ counter) {
+                    const float* __restrict__ W, const float* __restrict__ WT, float* __restrict__ H, int32_t n,
+                    int32_t m, int k, float lambda, const int32_t* __restrict__ col_order, int* __restrict__ counter) {
     __shared__ float s_num[kColThreadsL / 32], s_den[kColThreadsL / 32];
     __shared__ float s_z;
     __shared__ int s_j;
+    extern __shared__ __align__(16) float csm[];  // cached columns: [q][c][thread] gathered w of a chunk
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int tid = threadIdx.x;
+    const bool vec = (k & 3) == 0 && (kColChunk & 3) == 0;
     for (;;) {
         if (threadIdx.x == 0) s_j = atomicAdd(counter, 1);
         __syncthreads();
@@ -206,6 +251,77 @@ ccd_cols_lpt_kernel(const int64_t* __restrict__ col_start, const int32_t* __rest
         if (jj >= n) break;
         const int32_t j = col_order[jj];
         const int64_t b = col_start[j], e = col_start[j + 1];
+        if (e - b <= static_cast<int64_t>(kColThreadsL) * kColCache) {
+            // the column's residual in registers (kColCache per thread); the w of kColChunk coordinates
+            // gathered at once from the row-major W (one sector per entry and chunk)
+            float r[kColCache];
+            int32_t ii[kColCache];
+#pragma unroll
+            for (int c = 0; c < kColCache; ++c) {
+                const int64_t p = b + tid + static_cast<int64_t>(kColThreadsL) * c;
+                r[c] = p < e ? R[p] : 0.f;
+                ii[c] = p < e ? row_of[p] : -1;
+            }
+            for (int t0 = 0; t0 < k; t0 += kColChunk) {
+                const int cc = min(kColChunk, k - t0);
+#pragma unroll
+                for (int c = 0; c < kColCache; ++c) {
+                    if (ii[c] < 0) continue;
+                    const float* src = W + static_cast<int64_t>(ii[c]) * k + t0;
+                    if (vec && cc == kColChunk) {
+#pragma unroll
+                        for (int q = 0; q < kColChunk; q += 4) {
+                            const float4 v = *reinterpret_cast<const float4*>(src + q);
+                            csm[((q + 0) * kColCache + c) * kColThreadsL + tid] = v.x;
+                            csm[((q + 1) * kColCache + c) * kColThreadsL + tid] = v.y;
+                            csm[((q + 2) * kColCache + c) * kColThreadsL + tid] = v.z;
+                            csm[((q + 3) * kColCache + c) * kColThreadsL + tid] = v.w;
+                        }
+                    } else {
+                        for (int q = 0; q < cc; ++q) csm[(q * kColCache + c) * kColThreadsL + tid] = src[q];
+                    }
+                }
+                for (int tt = 0; tt < cc; ++tt) {
+                    const float hjt = H[static_cast<int64_t>(j) * k + t0 + tt];
+                    float num = 0.f, den = 0.f;
+                    float wc[kColCache];
+#pragma unroll
+                    for (int c = 0; c < kColCache; ++c) {
+                        wc[c] = ii[c] >= 0 ? csm[(tt * kColCache + c) * kColThreadsL + tid] : 0.f;
+                        if (ii[c] >= 0) {
+                            num = __fadd_rn(num, __fmul_rn(__fadd_rn(r[c], __fmul_rn(wc[c], hjt)), wc[c]));
+                            den = __fadd_rn(den, __fmul_rn(wc[c], wc[c]));
+                        }
+                    }
+                    warp_sum2(num, den);
+                    if (lane == 0) {
+                        s_num[warp] = num;
+                        s_den[warp] = den;
+                    }
+                    __syncthreads();
+                    if (warp == 0) {
+                        num = lane < kColThreadsL / 32 ? s_num[lane] : 0.f;
+                        den = lane < kColThreadsL / 32 ? s_den[lane] : 0.f;
+                        warp_sum2(num, den);
+                        if (lane == 0) {
+                            const float dt = __fadd_rn(lambda, den);
+                            s_z = dt == 0.f ? 0.f : __fdiv_rn(num, dt);
+                            H[static_cast<int64_t>(j) * k + t0 + tt] = s_z;
+                        }
+                    }
+                    __syncthreads();
+                    const float delta = __fsub_rn(s_z, hjt);
+#pragma unroll
+                    for (int c = 0; c < kColCache; ++c) r[c] = __fsub_rn(r[c], __fmul_rn(delta, wc[c]));
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < kColCache; ++c) {
+                const int64_t p = b + tid + static_cast<int64_t>(kColThreadsL) * c;
+                if (p < e) R[p] = r[c];
+            }
+            continue;
+        }
         float dprev = 0.f;
         for (int t = 0; t <= k; ++t) {
             const bool last = t == k;
@@ -322,7 +438,16 @@ void launch_ccd_xlinks(const int64_t* row_start, const int32_t* col_of, const in
 int launch_ccd_epoch(const CcdWs& ws, float* W, float* H, int k, float lambda, cudaStream_t s) {
     int launched = 0;
     if (ws.m > 0) {
-        ccd_rows_kernel<<<148 * 8, 256, 0, s>>>(ws.row_start, ws.col_of, ws.R_row, W, H, ws.m, k, lambda);
+        static const int per_sm = [] {
+            const int bytes = kRowSmemFloats * static_cast<int>(sizeof(float));
+            cudaFuncSetAttribute(ccd_rows_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            int n = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, ccd_rows_kernel, kRowThreads, bytes);
+            return std::max(n, 1);
+        }();
+        ccd_rows_kernel<<<148 * per_sm, kRowThreads, kRowSmemFloats * sizeof(float), s>>>(ws.row_start, ws.col_of,
+                                                                                          ws.R_row, W, H, ws.m, k,
+                                                                                          lambda);
         ++launched;
     }
     if (ws.nnz > 0) {
@@ -332,8 +457,15 @@ int launch_ccd_epoch(const CcdWs& ws, float* W, float* H, int k, float lambda, c
     if (ws.n > 0 && ws.WT) {
         ccd_transpose_kernel<<<dim3((ws.m + 31) / 32, (k + 31) / 32), dim3(32, 8), 0, s>>>(W, ws.WT, ws.m, k);
         cudaMemsetAsync(ws.counter, 0, sizeof(int), s);
-        ccd_cols_lpt_kernel<<<148 * (1024 / kColThreadsL), kColThreadsL, 0, s>>>(ws.col_start, ws.row_of, ws.R_col, ws.WT, H, ws.n, ws.m, k,
-                                                         lambda, ws.col_order, ws.counter);
+        static const int col_per_sm = [] {
+            const int bytes = kColSmemFloats * static_cast<int>(sizeof(float));
+            cudaFuncSetAttribute(ccd_cols_lpt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+            int nb = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, ccd_cols_lpt_kernel, kColThreadsL, bytes);
+            return std::max(1, std::min(nb, 1024 / kColThreadsL));
+        }();
+        ccd_cols_lpt_kernel<<<148 * col_per_sm, kColThreadsL, kColSmemFloats * sizeof(float), s>>>(
+            ws.col_start, ws.row_of, ws.R_col, W, ws.WT, H, ws.n, ws.m, k, lambda, ws.col_order, ws.counter);
         launched += 2;
     } else if (ws.n > 0) {
         ccd_cols_kernel<<<148 * 8, kColThreads, 0, s>>>(ws.col_start, ws.row_of, ws.R_col, W, H, ws.n, k, lambda);
