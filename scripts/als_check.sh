@@ -3,12 +3,6 @@ timeout 150 python -m pytest tests/test_gpu_als.py tests/test_gpu_ccdw.py -q -x 
 for cfg in netflix-als ml10m-als; do
   timeout 120 python bench.py --config $cfg --no-extra --no-cpu-baseline --no-e2e --steps 5 --warmup 2 > gpurun_out/als_$cfg.json 2> gpurun_out/als_$cfg.err
 done
-if [ -f scripts/_variants/libpmf_gpu_nosolve.so ]; then
-  cp paper_1511_02433_b200/libpmf_gpu.so /tmp/keep.so
-  cp scripts/_variants/libpmf_gpu_nosolve.so paper_1511_02433_b200/libpmf_gpu.so
-  timeout 120 python bench.py --config netflix-als --no-extra --no-cpu-baseline --no-e2e --steps 5 --warmup 2 > gpurun_out/als_nosolve.json 2>/dev/null
-  cp /tmp/keep.so paper_1511_02433_b200/libpmf_gpu.so
-fi
 if [ -n "$NCU" ]; then
   timeout 300 ncu --set full --import-source on --clock-control none -k regex:als_umma -c 2 -o gpurun_out/prof_umma -f python bench.py --config netflix-als --no-extra --no-cpu-baseline --no-e2e --steps 1 --warmup 1 > gpurun_out/ncu_umma.log 2>&1
 fi
