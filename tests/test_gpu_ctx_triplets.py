@@ -126,3 +126,9 @@ def test_netflix_shape_bitwise(pmf):
     _same(host, dev)
     host.close()
     dev.close()
+
+
+def test_large_k_bitwise(pmf, ml100k):
+    """k > 64: ALS on the CTA-per-system path (als_big_kernels.cu) reads the device CSR / CSC the same way."""
+    train, probe = ml100k
+    _run_all(pmf, train, 943, 1682, 72, probe, ccd=False)
