@@ -131,3 +131,21 @@ def test_dist_plan_edge_cases(pmf):
     assert list(rb1) == [0, 5] and Bm1 == 5 and Bn1 == 4
     with pytest.raises(ValueError):
         pmf.dist_plan(A, 0)
+
+
+def test_bench_relaunches_ranks_for_the_reference_arm():
+    """bench.py --gpus 2 outside torchrun relaunches itself as 2 ranks (torch.distributed.run, 127.0.0.1);
+    the reference arm runs on rank 0 only and prints exactly one JSON line (CPU, gloo)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--config", "ml100k-ccdpp", "--steps", "1", "--warmup", "0"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert p.returncode == 0, p.stderr[-2000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["impl"] == "reference" and d["value"] > 0 and d["e2e"]["h2d_bytes_per_step"] == 0
