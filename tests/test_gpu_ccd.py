@@ -328,7 +328,8 @@ def test_set_model_rebuilds_residual(pmf, oracle, ml100k):
     ref.close(); ctx.close()
 
 
-def test_small_path_matches_graph_schedule(ml100k):
+@pytest.mark.parametrize("k,T", [(10, 15), (1, 1), (33, 2)])
+def test_small_path_matches_graph_schedule(ml100k, k, T):
     """ML-100K runs its whole outer iteration as one cluster kernel (small_kernels.cu); PMF_SMALL=0 keeps
     the CUDA-graph schedule of the large shapes.  Same layouts and per-entry arithmetic, different sum
     order: the trajectories agree to FP32 rounding, and each keeps its two residual copies bitwise equal
@@ -348,7 +349,7 @@ train, probe = O.carve_probe(a, 10000, 5)
 A = P.RatingsMatrix.from_triplets(train, 943, 1682)
 ctx = P.Context(A)
 ctx.set_probe(probe)
-ctx.ccdpp_begin(P.CcdConfig(k=10, lam=0.05, outer_iters=3, inner_iters=15, seed=1))
+ctx.ccdpp_begin(P.CcdConfig(k=int(sys.argv[2]), lam=0.05, outer_iters=3, inner_iters=int(sys.argv[3]), seed=1))
 rows = []
 for _ in range(3):
     ctx.ccdpp_iterate(1)
@@ -358,11 +359,11 @@ print(json.dumps({"rows": rows, "launches": ctx.launch_count()}))
     from conftest import ROOT
     out = {}
     for flag in ("1", "0"):
-        r = subprocess.run([sys.executable, "-c", code, ROOT], env=dict(os.environ, PMF_SMALL=flag),
+        r = subprocess.run([sys.executable, "-c", code, ROOT, str(k), str(T)], env=dict(os.environ, PMF_SMALL=flag),
                            capture_output=True, text=True, timeout=240)
         assert r.returncode == 0, r.stderr[-2000:]
         out[flag] = json.loads(r.stdout.strip().splitlines()[-1])
-    assert out["1"]["launches"] == 1 and out["0"]["launches"] > 100
+    assert out["1"]["launches"] == 1 and out["0"]["launches"] > 2 * T * k - 1
     for a, b in zip(out["1"]["rows"], out["0"]["rows"]):
         for x, y in zip(a, b):
             assert abs(x - y) <= 1e-5 * abs(y)
