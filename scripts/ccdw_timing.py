@@ -12,7 +12,8 @@ import paper_1511_02433_b200 as P  # noqa: E402
 for cfg in ("netflix-ccdpp", "ml10m-als"):
     m, n, ntr, npr, k, *_ = bench.CONFIGS[cfg]
     k = 40 if cfg.startswith("netflix") else 10
-    train, probe, A = bench.make_data(cfg)
+    train, probe = bench.make_data(cfg)
+    A = P.RatingsMatrix.from_triplets(train, *bench.CONFIGS[cfg][:2])
     ctx = P.Context(A)
     ctx.ccd_begin(P.CcdConfig(k=k, lam=0.05, outer_iters=3, inner_iters=1, seed=1))
     secs = ctx.ccd_iterate(3)

@@ -30,7 +30,8 @@ def main():
     oa = int(os.environ.get("OUTER_ALS", "2"))
     cfg = os.environ.get("CONFIG", "netflix-ccdpp")
     m, n, _, _, k, *_ = bench.CONFIGS[cfg]
-    train, probe, A = bench.make_data(cfg)
+    train, probe = bench.make_data(cfg)
+    A = P.RatingsMatrix.from_triplets(train, *bench.CONFIGS[cfg][:2])
     ref = Reference()
     workers = os.cpu_count() or 1
     RA = RefMatrix(ref, train, m, n, "_f32")
@@ -51,11 +52,13 @@ def main():
             os.environ.pop("PMF_CCD_GRAM", None)
         t_gpu = time.time() - t0
         t0 = time.time()
+        # the stage-API loop / epoch loop: bitwise the reference's ccdpp_train / als_train trajectory
+        # (tests/test_oracle.py) and their rows also carry the train RMSE
         if algo == "ccdpp":
-            W, H, rows = RA.ccdpp_train(k, 0.05, oc, 15, 1, probe, workers)
+            W, H, rows, _, _ = RA.ccdpp_stage_loop(k, 0.05, oc, 15, 1, probe, workers)
         elif algo == "als":
-            W, H, rows = RA.als_train(k, 0.05, oa, 1, probe, workers)
-        elif "ccd" not in ref_cache:
+            W, H, rows = RA.als_epochs(k, 0.05, oa, 1, probe, workers)
+        elif "ccd" not in ref_cache:  # (ccd_train's rows have no train RMSE: the final one is compared)
             W, H, rows = ref_cache["ccd"] = RA.ccd_train(k, 0.05, ow, 1, probe)
         else:
             W, H, rows = ref_cache["ccd"]
@@ -69,7 +72,11 @@ def main():
             print(f"{algo} iter {r.iteration}: objective {r.objective:.8g} vs {float(g['objective']):.8g} "
                   f"(rel {its[-1]['rel_objective']:.2e}), probe rmse rel {its[-1]['rel_probe_rmse']:.2e}, "
                   f"train rmse rel {its[-1]['rel_train_rmse']:.2e}", flush=True)
+        # final train RMSE of both models, evaluated by the same (reference-pinned) rmse kernel
+        tr_gpu = P.rmse(model, train)
+        tr_ref = P.rmse(P.FactorModel(np.ascontiguousarray(W, np.float32), np.ascontiguousarray(H, np.float32)), train)
         out[algo] = {"iterations": its, "frob_rel_W": frob(model.w, W), "frob_rel_H": frob(model.h, H),
+                     "final_train_rmse": [tr_gpu, tr_ref], "rel_final_train_rmse": rel(tr_gpu, tr_ref),
                      "gpu_wall_s": round(t_gpu, 2), "reference_wall_s": round(t_ref, 2)}
         print(f"{algo}: factors rel Frobenius W {out[algo]['frob_rel_W']:.2e} H {out[algo]['frob_rel_H']:.2e}; "
               f"wall GPU {t_gpu:.1f} s (incl. setup) vs reference {t_ref:.1f} s", flush=True)

@@ -16,7 +16,8 @@ from oracle.pyoracle import Reference  # noqa: E402
 
 
 def main():
-    train, probe, A = bench.make_data("netflix-ccdpp")
+    train, probe = bench.make_data("netflix-ccdpp")
+    A = P.RatingsMatrix.from_triplets(train, *bench.CONFIGS["netflix-ccdpp"][:2])
     model, _ = P.ccdpp_train(P.CcdConfig(k=40, lam=0.05, outer_iters=2, inner_iters=15, seed=1), A, probe)
     rng = np.random.default_rng(5)
     users = np.sort(rng.choice(A.m, 200, replace=False)).astype(np.int32)
