@@ -14,7 +14,8 @@ import paper_1511_02433_b200 as P  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="yahoo-ccdpp")
 a = ap.parse_args()
-train, probe, A = bench.make_data(a.config)
+train, probe = bench.make_data(a.config)
+A = P.RatingsMatrix.from_triplets(train, *bench.CONFIGS[a.config][:2])
 ctx = P.Context(A)
 ctx.ccdpp_begin(P.CcdConfig(k=2, lam=0.05, outer_iters=1, inner_iters=15, seed=1))
 ctx.ccdpp_iterate(1)

@@ -11,7 +11,8 @@ sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 import paper_1511_02433_b200 as P  # noqa: E402
 
-train, probe, A = bench.make_data("netflix-ccdpp")
+train, probe = bench.make_data("netflix-ccdpp")
+A = P.RatingsMatrix.from_triplets(train, *bench.CONFIGS["netflix-ccdpp"][:2])
 rng = np.random.default_rng(1)
 model = P.FactorModel(rng.normal(0, 0.3, (A.m, 40)).astype(np.float32), rng.normal(0, 0.3, (A.n, 40)).astype(np.float32))
 users = np.arange(A.m, dtype=np.int32)
