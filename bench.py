@@ -165,7 +165,9 @@ def ccd_epoch_roofline(N, k, seconds, hbm):
     b = 2 * k * 8 * N
     return {"bound": "hbm", "achieved": round(b / seconds / 1e9, 1), "unit": "GB/s", "peak": hbm,
             "frac": round(b / seconds / 1e9 / hbm, 4), "algorithmic_bytes_per_epoch": b,
-            "note": "latency-bound (per-coordinate dependent gathers); the column sweep claims columns longest first"}
+            "note": "latency-bound: a coordinate-by-coordinate chain per row / column; rows and columns up to 8K "
+                    "entries keep their residual in registers and gather the opposing factor 8 / 4 coordinates "
+                    "at a time, longer columns stream (profiles/r02_ncu_ccdw.txt)"}
 
 
 def barrier(dist):
